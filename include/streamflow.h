@@ -1,0 +1,149 @@
+/*
+ * streamflow.h -- C ABI of the B200-native StreamFlow stream-batch hot path.
+ *
+ * The reference (`flowpipe`, /root/reference/pkg/src/flowpipe) is a pure
+ * Python/numpy package with no FFI; its boundary is a Python API.  This header
+ * is the native boundary our Python drop-in (package `paper_2511_22009_b200`)
+ * binds with ctypes; every entry point names the reference function it
+ * replaces (file:line, relative to pkg/src/flowpipe/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ *    owned by the caller; the library never allocates device memory on the
+ *    hot path (the DiT runtime handle holds host-side state only).
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered,
+ *    asynchronous and reentrant.
+ *  - Return value: SF_OK (0) or a negative SF_ERR_* code.  Error kinds map to
+ *    the reference's exception classes (errors.py:4-39).  Data-dependent
+ *    checks (off-grid t, non-positive window denominator) are reported through
+ *    a device-side `status` word with the SF_STATUS_* bits; the caller reads it
+ *    when it needs to raise.
+ */
+#ifndef STREAMFLOW_H_
+#define STREAMFLOW_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status / error codes (errors.py:4-39) ---- */
+#define SF_OK 0
+#define SF_ERR_PARAMETER (-1)   /* ParameterError   (errors.py:8)  */
+#define SF_ERR_TIME_DOMAIN (-2) /* TimeDomainError  (errors.py:12) */
+#define SF_ERR_INVARIANT (-3)   /* InvariantError   (errors.py:24) */
+#define SF_ERR_STATE (-4)       /* StateError       (errors.py:16) */
+#define SF_ERR_CUDA (-5)        /* CUDA launch / driver failure    */
+
+#define SF_STATUS_TIME_RANGE 1u /* t outside [0,1]        schedule.py:195-198 */
+#define SF_STATUS_OFF_GRID 2u   /* t not on the grid      schedule.py:279-283 */
+#define SF_STATUS_DENOM 4u      /* denominator <= 0       schedule.py:248-252 */
+
+/* ---- dtypes ---- */
+#define SF_F32 0
+#define SF_F64 1
+#define SF_BF16 2
+
+/* Per-row step coefficients written by sf_window_params: SF_PARAM_STRIDE
+ * doubles per row, in this order. */
+#define SF_P_T 0
+#define SF_P_TNEXT 1
+#define SF_P_TS 2
+#define SF_P_TE 3
+#define SF_P_GAMMA 4
+#define SF_P_LAMBDA_S 5
+#define SF_P_ETA_S 6
+#define SF_P_LAMBDA_T 7
+#define SF_P_ETA_T 8
+#define SF_P_SPAN 9
+#define SF_P_DT 10
+#define SF_P_AT_END 11 /* 1.0 / 0.0 */
+#define SF_PARAM_STRIDE 12
+
+/* Device-resident scheduler arguments (schedule.py:87-133): boundaries
+ * [num_windows+1], abar [t_max], grid [num_steps], all fp64 device arrays. */
+typedef struct sf_schedule {
+  const double* boundaries;
+  const double* abar;
+  const double* grid;
+  int32_t num_windows;
+  int32_t t_max;
+  int32_t num_steps;
+  int32_t _pad;
+  double eps;
+} sf_schedule;
+
+const char* sf_version(void);
+int sf_device_sm_count(void);
+
+/* K1 -- window coefficients + grid successor for B flow times.
+ * Replaces window_params (schedule.py:224-263), window_lookup (:208-221),
+ * alpha_bar_index (:201-205), next_timestep / grid_indices (:266-295).
+ * out: [B, SF_PARAM_STRIDE] fp64.  status: device uint32, OR-ed SF_STATUS_*.
+ * Off-grid rows get t_next = NaN (the caller raises TimeDomainError). */
+int sf_window_params(const sf_schedule* sched, const double* ts, int64_t B, double* out, uint32_t* status,
+                     void* stream);
+
+/* K10-lite -- heterogeneous-t Euler step, bit-exact with numpy.
+ * Replaces batched_velocity_step (velocity.py:93-135).
+ * eps: [B, D] of eps_dtype (F32/F64); x, x_out: [B, D] of x_dtype (F32/F64);
+ * params: [B, SF_PARAM_STRIDE] from sf_window_params.  x_out may alias x. */
+int sf_velocity_step(const void* eps, int eps_dtype, const void* x, void* x_out, int x_dtype, const double* params,
+                     int64_t B, int64_t D, void* stream);
+
+/* CFG combine: out[i] = e[i] + w * (e[i+B] - e[i]) over a [2B, D] block.
+ * Replaces handle_cfg (models.py:278-296); fp64 or fp32. */
+int sf_cfg_combine(const void* eps2, int dtype, int64_t B, int64_t D, double w, void* out, void* stream);
+
+/* K12 -- seeded mock velocity model (models.py:199-241).
+ * sf_mock_keys: blake2b-64 row keys of (model_seed, ids[i], round(ts[i]*1e9),
+ *   row_embs[i, :E]) (models.py:223-228).  row_embs: [B, E] fp64.
+ * sf_mock_eps: splitmix64 expansion of each key into D fp64 values in
+ *   [-1, 1) (models.py:188-196), out [B, D]. */
+int sf_mock_keys(int64_t model_seed, const int64_t* ids, const double* ts, const double* row_embs, int64_t B,
+                 int32_t E, uint64_t* keys, void* stream);
+int sf_mock_eps(const uint64_t* keys, int64_t B, int64_t D, double* out, void* stream);
+
+/* ---- device-resident stream batch (pipeline.py:139-220) ----
+ * S independent streams x n in-flight slots.  Ring row r = s*n + k holds the
+ * generation g of stream s with g = k (mod n); at iteration j its stage is
+ * (j - k) mod n and it is active iff 0 <= g < m.  The
+ * queue shift is the implicit advance of j; nothing moves in memory.
+ *
+ * ctl: device int64[4]: [0] = next iteration j, [1] = iteration being run.
+ * stage_params: [n, SF_PARAM_STRIDE] (sf_window_params of grid[:n]).
+ * row_info: device int64[S*n*4] written by sf_stream_prepare:
+ *   [r*4+0] stage, [r*4+1] gen id, [r*4+2] active, [r*4+3] stream.
+ * row_t: device fp64[S*n] flow time of each ring row. */
+int sf_stream_prepare(int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params, int64_t* row_info,
+                      double* row_t, void* stream);
+
+/* Mock-model stream step: guided mock eps (CFG fused when w != 1) + Euler on
+ * every active ring row + emission of retiring rows + refill of the slot that
+ * admits generation j+1.
+ *   x_ring [S*n, D] (x_dtype), frames_out [S, D] (x_dtype), frame_ids [S]
+ *   (-1 when nothing retired this iteration), noise_in [S, D] fp64: initial
+ *   noise of generation j+1 per stream (pipeline.py:92-98), ignored when
+ *   j+1 >= m.  emb / neg: [S, E] fp64 (neg may be NULL = zeros,
+ *   models.py:258-260).  model_seed: SeededMockModel seed. */
+int sf_stream_mock_step(const int64_t* ctl, int64_t S, int32_t n, int64_t m, int64_t D, int x_dtype, void* x_ring,
+                        const double* stage_params, const int64_t* row_info, const double* row_t, int64_t model_seed,
+                        const double* emb, const double* neg, int32_t E, double w, const double* noise_in,
+                        void* frames_out, int64_t* frame_ids, void* stream);
+
+/* Write generation-0 noise into slot 0 of every stream and reset ctl (j = 0). */
+int sf_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, int x_dtype, void* x_ring,
+                    const double* noise0, void* stream);
+
+/* ---- tcgen05 GEMM (DiT dense contractions) ----
+ * C[M, N] = A[M, K] . W[N, K]^T + bias, bf16 in, fp32 accumulate.
+ * epi: 0 = f32 out, 1 = bf16 out, 2 = bf16 GELU(tanh) out.
+ * K % 64 == 0, N % 128 == 0 (N % 256 == 0 uses 256-wide tiles). */
+int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
+                 int32_t epi, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STREAMFLOW_H_ */

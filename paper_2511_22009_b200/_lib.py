@@ -1,0 +1,100 @@
+"""ctypes binding of ``libstreamflow.so`` (the C ABI in ``include/streamflow.h``).
+
+There is no fallback: if the library is missing or a CUDA device is absent,
+every compute entry point raises.  The product path never runs on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from .errors import InvariantError, ParameterError, StateError, TimeDomainError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstreamflow.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "streamflow.h")
+
+SF_OK = 0
+SF_ERR_PARAMETER, SF_ERR_TIME_DOMAIN, SF_ERR_INVARIANT, SF_ERR_STATE, SF_ERR_CUDA = -1, -2, -3, -4, -5
+SF_STATUS_TIME_RANGE, SF_STATUS_OFF_GRID, SF_STATUS_DENOM = 1, 2, 4
+SF_F32, SF_F64, SF_BF16 = 0, 1, 2
+(P_T, P_TNEXT, P_TS, P_TE, P_GAMMA, P_LAMBDA_S, P_ETA_S, P_LAMBDA_T, P_ETA_T,
+ P_SPAN, P_DT, P_AT_END) = range(12)
+PARAM_STRIDE = 12
+
+
+class SfSchedule(C.Structure):
+    _fields_ = [
+        ("boundaries", C.c_void_p), ("abar", C.c_void_p), ("grid", C.c_void_p),
+        ("num_windows", C.c_int32), ("t_max", C.c_int32), ("num_steps", C.c_int32),
+        ("_pad", C.c_int32), ("eps", C.c_double),
+    ]
+
+
+_vp, _i64, _i32, _f64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+
+# name -> argtypes (restype is int unless stated)
+SIGNATURES = {
+    "sf_version": [],
+    "sf_device_sm_count": [],
+    "sf_window_params": [C.POINTER(SfSchedule), _vp, _i64, _vp, _vp, _vp],
+    "sf_velocity_step": [_vp, C.c_int, _vp, _vp, C.c_int, _vp, _i64, _i64, _vp],
+    "sf_cfg_combine": [_vp, C.c_int, _i64, _i64, _f64, _vp, _vp],
+    "sf_mock_keys": [_i64, _vp, _vp, _vp, _i64, _i32, _vp, _vp],
+    "sf_mock_eps": [_vp, _i64, _i64, _vp, _vp],
+    "sf_stream_prepare": [_vp, _i64, _i32, _i64, _vp, _vp, _vp, _vp],
+    "sf_stream_mock_step": [_vp, _i64, _i32, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _i64,
+                            _vp, _vp, _i32, _f64, _vp, _vp, _vp, _vp],
+    "sf_stream_reset": [_vp, _i64, _i32, _i64, C.c_int, _vp, _vp, _vp],
+    "sf_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp],
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares (``int sf_xxx(`` / ``const char* sf_xxx(``)."""
+    with open(HEADER) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sf_\w+)\s*\(", text, re.M)))
+
+
+def load():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2511_22009_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_char_p if name == "sf_version" else C.c_int
+    _lib = lib
+    return lib
+
+
+_ERRS = {
+    SF_ERR_PARAMETER: ParameterError,
+    SF_ERR_TIME_DOMAIN: TimeDomainError,
+    SF_ERR_INVARIANT: InvariantError,
+    SF_ERR_STATE: StateError,
+}
+
+
+def check(code: int, what: str) -> None:
+    if code == SF_OK:
+        return
+    exc = _ERRS.get(code)
+    if exc is not None:
+        raise exc(f"{what}: rejected by libstreamflow (code {code})")
+    raise RuntimeError(f"{what}: CUDA failure in libstreamflow (code {code})")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

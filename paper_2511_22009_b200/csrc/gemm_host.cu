@@ -1,0 +1,75 @@
+// Host side of the tcgen05 GEMM: TMA descriptor encoding + launch dispatch.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm_tcgen05.cuh"
+#include "sf_internal.h"
+
+namespace sf {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Row-major bf16 matrix [outer, inner] -> 2-D tiled map with a (box_inner x
+// box_outer) box and 128-byte swizzle (box_inner * 2 must be 128).
+int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                      uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return SF_ERR_CUDA;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SF_OK : SF_ERR_CUDA;
+}
+
+template <int BN, int KIND>
+static int launch_one(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, const EpiParams& ep,
+                      cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES) != cudaSuccess)
+      return SF_ERR_CUDA;
+    attr_done = true;
+  }
+  dim3 grid(N / BN, (M + C::BM - 1) / C::BM);
+  gemm_bf16_tcgen05<BN, KIND><<<grid, 192, C::SMEM_BYTES, st>>>(a, b, K, ep);
+  return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+}
+
+int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
+
+int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                const EpiParams& ep, cudaStream_t st) {
+  if (K % 64 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
+#define SF_CASE(BN_, KIND_) \
+  if (bn == BN_ && kind == KIND_) return launch_one<BN_, KIND_>(a, b, M, N, K, ep, st);
+  SF_CASE(128, EPI_F32)
+  SF_CASE(128, EPI_BF16)
+  SF_CASE(128, EPI_GELU)
+  SF_CASE(256, EPI_F32)
+  SF_CASE(256, EPI_BF16)
+  SF_CASE(256, EPI_GELU)
+  SF_CASE(192, EPI_QKV)
+  SF_CASE(384, EPI_RES_LN)
+#undef SF_CASE
+  return SF_ERR_PARAMETER;
+}
+
+}  // namespace sf

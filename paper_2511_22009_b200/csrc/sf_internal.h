@@ -1,0 +1,17 @@
+// Internal declarations shared by the .cu translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/streamflow.h"
+
+namespace sf {
+struct EpiParams;
+int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                      uint32_t box_inner, uint32_t box_outer);
+int gemm_b_box_rows(int bn);
+int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                const EpiParams& ep, cudaStream_t st);
+
+inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
+}  // namespace sf
