@@ -49,6 +49,10 @@ SIGNATURES = {
                             _vp, _vp, _i32, _f64, _vp, _vp, _vp, _vp],
     "sf_stream_reset": [_vp, _i64, _i32, _i64, C.c_int, _vp, _vp, _vp],
     "sf_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp],
+    "sf_gemm_qkv": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, C.c_float, _vp],
+    "sf_gemm_res_ln": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32,
+                       C.c_float, _vp],
+    "sf_attention": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
 }
 
 _lib = None

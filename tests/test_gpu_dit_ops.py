@@ -1,0 +1,90 @@
+"""DiT building blocks on sm_100a vs plain torch fp32 references of the same op:
+QKV GEMM with head-major scatter, gated-residual + LayerNorm + modulate
+epilogue, and tcgen05 flash attention."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def L():
+    from paper_2511_22009_b200 import _lib
+    return _lib
+
+
+def st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("rows", [1, 3])
+def test_qkv_scatter(rows):
+    T, H = 1024, 6
+    d = H * 64
+    M = rows * T
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    a = bf(torch.randn(M, d, device="cuda", generator=g))
+    w = bf(torch.randn(3 * d, d, device="cuda", generator=g) * 0.05)
+    b = torch.randn(3 * d, device="cuda", generator=g) * 0.1
+    q = torch.empty(rows, H, T, 64, device="cuda", dtype=torch.bfloat16)
+    k = torch.empty_like(q)
+    vt = torch.empty(rows, H, 64, T, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_gemm_qkv", a.data_ptr(), w.data_ptr(), b.data_ptr(), q.data_ptr(), k.data_ptr(),
+             vt.data_ptr(), M, H, T, 0.125, st())
+    torch.cuda.synchronize()
+    ref = (a.float() @ w.float().t() + b).view(rows, T, 3, H, 64)
+    rq = ref[:, :, 0].permute(0, 2, 1, 3) * 0.125
+    rk = ref[:, :, 1].permute(0, 2, 1, 3)
+    rv = ref[:, :, 2].permute(0, 2, 3, 1)
+    for got, want in ((q, rq), (k, rk), (vt, rv)):
+        assert (got.float() - want).abs().max().item() < 2e-2 * max(1.0, want.abs().max().item())
+
+
+@pytest.mark.parametrize("K", [384, 1536])
+def test_res_ln_epilogue(K):
+    rows, T, N = 2, 1024, 384
+    M = rows * T
+    g = torch.Generator(device="cuda").manual_seed(K)
+    a = bf(torch.randn(M, K, device="cuda", generator=g))
+    w = bf(torch.randn(N, K, device="cuda", generator=g) * 0.05)
+    b = torch.randn(N, device="cuda", generator=g) * 0.1
+    xres = bf(torch.randn(M, N, device="cuda", generator=g))
+    x0 = xres.float().clone()
+    vec_stride = 4 * N
+    vecs = torch.randn(rows, vec_stride, device="cuda", generator=g) * 0.5
+    gate, shift, scale = vecs[:, 0:N], vecs[:, N:2 * N], vecs[:, 2 * N:3 * N]
+    xmod = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_gemm_res_ln", a.data_ptr(), w.data_ptr(), b.data_ptr(), xres.data_ptr(),
+             xmod.data_ptr(), gate.data_ptr(), shift.data_ptr(), scale.data_ptr(), vec_stride,
+             M, N, K, T, 1e-6, st())
+    torch.cuda.synchronize()
+    slot = torch.arange(M, device="cuda") // T
+    y = x0 + gate[slot] * (a.float() @ w.float().t() + b)
+    assert (xres.float() - y).abs().max().item() < 3e-2 * max(1.0, y.abs().max().item())
+    ln = torch.nn.functional.layer_norm(y, (N,), eps=1e-6)
+    ref = ln * (1 + scale[slot]) + shift[slot]
+    assert (xmod.float() - ref).abs().max().item() < 5e-2 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("rows,H,scale", [(1, 6, 1.0), (2, 6, 4.0), (1, 16, 8.0)])
+def test_attention_matches_sdpa(rows, H, scale):
+    T = 1024
+    g = torch.Generator(device="cuda").manual_seed(rows * H)
+    q = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g) * scale / 8)
+    k = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g))
+    v = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g))
+    vt = v.transpose(-1, -2).contiguous()
+    out = torch.empty(rows * T, H * 64, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_attention", q.data_ptr(), k.data_ptr(), vt.data_ptr(), out.data_ptr(), rows, H, T, st())
+    torch.cuda.synchronize()
+    # q already carries the 1/sqrt(d) factor -> sdpa with scale=1
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float(), scale=1.0)
+    ref = ref.permute(0, 2, 1, 3).reshape(rows * T, H * 64)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
