@@ -163,6 +163,75 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
 int sf_attention(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads, int32_t T,
                  void* stream);
 
+/* ---- DiT velocity-field runtime (the network behind VelocityModel.forward,
+ * models.py:89-136; it has no reference implementation -- SURVEY 8(c)) ----
+ * DiT-S/2 geometry: hidden 384, 6 heads of 64, depth 12, patch 2, 4 latent
+ * channels, 64x64 latent (1024 tokens), MLP 1536, 256 sinusoid features,
+ * conditioning vector of embed_dim (8).  Weights are bf16 [out, in]
+ * row-major unless marked (t), which are transposed [in, out]; biases fp32. */
+typedef struct sf_dit_config {
+  int32_t depth, hidden, heads, patch, in_ch, latent_hw, embed_dim, freq_dim, mlp_hidden;
+  float ln_eps;
+} sf_dit_config;
+
+typedef struct sf_dit_weights {
+  const void* patch_w;    /* bf16 [hidden, in_ch*p*p]  (Conv2d weight, (c,p,q) order) */
+  const float* patch_b;   /* [hidden] */
+  const float* pos_embed; /* [tokens, hidden] fixed 2-D sin-cos */
+  const void* t_w1t;      /* bf16 (t) [freq_dim, hidden] */
+  const float* t_b1;
+  const void* t_w2t;      /* bf16 (t) [hidden, hidden] */
+  const float* t_b2;
+  const void* y_wt;       /* bf16 (t) [embed_dim, hidden] */
+  const float* y_b;
+  const void* ada_w;      /* bf16 [depth*6*hidden + 2*hidden, hidden]: every block's adaLN then the final's */
+  const float* ada_b;
+  const void* qkv_w;      /* bf16 [depth, 3*hidden, hidden] */
+  const float* qkv_b;     /* [depth, 3*hidden] */
+  const void* proj_w;     /* bf16 [depth, hidden, hidden] */
+  const float* proj_b;
+  const void* fc1_w;      /* bf16 [depth, mlp_hidden, hidden] */
+  const float* fc1_b;
+  const void* fc2_w;      /* bf16 [depth, hidden, mlp_hidden] */
+  const float* fc2_b;
+  const void* final_w;    /* bf16 [p*p*in_ch, hidden]; output feature f = (p*P+q)*C + c */
+  const float* final_b;
+} sf_dit_weights;
+
+typedef struct sf_dit sf_dit; /* opaque runtime handle (host state + TMA descriptors + graph cache) */
+
+int64_t sf_dit_workspace_bytes(const sf_dit_config* cfg, int64_t max_rows);
+int sf_dit_mod_stride(const sf_dit_config* cfg);
+int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max_rows, void* workspace,
+                  int64_t ws_bytes, sf_dit** out);
+int sf_dit_destroy(sf_dit* h);
+
+/* One velocity-field evaluation (VelocityModel.forward, models.py:111-114):
+ * x [rows, in_ch, hw, hw] fp32, ts [rows] fp64 flow times (model time 1000 t),
+ * row_embs [rows, embed_dim] fp64 -> eps_out [rows, in_ch*hw*hw] fp32. */
+int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, const double* row_embs, float* eps_out,
+                   void* stream);
+
+/* One stream-batch iteration with the DiT (pipeline.py:171-219) fully on device:
+ * ring bookkeeping, one guided velocity evaluation over all S*n slots (2x rows
+ * when w != 1, models.py:244-296), fused CFG + Euler + emit + refill on the
+ * fp32 ring x_ring [S*n, D].  noise_in [S, D] fp32 = initial noise of
+ * generation j+1 per stream, or NULL for on-device Philox(noise_seed + s).
+ * use_graph != 0 captures the launch sequence into a CUDA graph on first use
+ * (keyed by the buffer pointers) and replays it afterwards. */
+int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
+                       int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
+                       const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                       int32_t use_graph, void* stream);
+
+/* Reset a fp32 ring: generation-0 noise into slot 0 of each stream (noise0 [S, D]
+ * or Philox when NULL), ctl <- j = 0. */
+int sf_dit_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, float* x_ring, const float* noise0,
+                        uint64_t noise_seed, void* stream);
+
+/* On-device N(0,1) noise: out[s, i] = Philox(seed + s, gen, i) (Box-Muller). */
+int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t gen, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

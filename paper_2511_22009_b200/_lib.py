@@ -65,6 +65,9 @@ def header_symbols() -> list[str]:
     return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sf_\w+)\s*\(", text, re.M)))
 
 
+RESTYPES = {"sf_version": C.c_char_p, "sf_dit_workspace_bytes": C.c_int64}
+
+
 def load():
     """Load the shared library (raises if it was not built)."""
     global _lib
@@ -74,13 +77,17 @@ def load():
         raise RuntimeError(
             f"{LIB_PATH} is missing: build it with `python -m paper_2511_22009_b200.build` "
             "(there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
-    for name, args in SIGNATURES.items():
-        fn = getattr(lib, name)
-        fn.argtypes = args
-        fn.restype = C.c_char_p if name == "sf_version" else C.c_int
-    _lib = lib
-    return lib
+    _lib = C.CDLL(LIB_PATH)
+    return _lib
+
+
+def fn(name: str):
+    """The library function ``name`` with its ctypes signature applied."""
+    f = getattr(load(), name)
+    if name in SIGNATURES and f.argtypes is None:
+        f.argtypes = SIGNATURES[name]
+        f.restype = RESTYPES.get(name, C.c_int)
+    return f
 
 
 _ERRS = {
@@ -101,4 +108,4 @@ def check(code: int, what: str) -> None:
 
 
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    check(fn(name)(*args), name)

@@ -249,10 +249,6 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc<attn::TMEM_COLS>(tmem);
 }
 
-struct AttnMaps {
-  CUtensorMap q, k, v;
-};
-
 int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T) {
   const uint64_t bhT = (uint64_t)rows * heads * T;
   if (make_tmap_bf16_2d(&m->q, q, 64, bhT, 64, 64, attn::BQ) != SF_OK) return SF_ERR_CUDA;

@@ -1,0 +1,634 @@
+// DiT velocity-field runtime: the per-step launch sequence of the stream batch.
+//
+//   prepare (K11 ring bookkeeping) -> cond (K1: t-embed MLP + y-embed + SiLU)
+//   -> adaLN GEMM (K3, all blocks at once) -> patch-embed + pos + LN1 (K2/K4)
+//   -> 12 x [QKV GEMM (K5) -> flash attention (K6) -> proj GEMM + gated
+//            residual + LN2 (K7+K4) -> fc1 GEMM + GELU (K8) -> fc2 GEMM +
+//            gated residual + next LN (K9+K4)]
+//   -> final layer fused with CFG combine + Euler + emit + refill (K10+K11)
+//
+// The handle owns host-side state only (config, TMA descriptors, graph
+// cache).  All device memory (weights, workspace, ring state) is owned by the
+// caller and passed as raw pointers.
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "gemm_tcgen05.cuh"
+#include "sf_internal.h"
+
+namespace sf {
+
+// ============================================================ shared helpers
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+// N(0,1) sample #idx of generation `gen` of a stream seeded `seed` (Philox + Box-Muller).
+__device__ __forceinline__ float philox_normal(uint64_t seed, int64_t gen, int64_t idx) {
+  const uint4 r = philox4x32(make_uint4((uint32_t)(idx >> 2), (uint32_t)gen, (uint32_t)(gen >> 32), 0x5f1u),
+                             make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const int lane = idx & 3;
+  const uint32_t a = (lane < 2) ? r.x : r.z, b = (lane < 2) ? r.y : r.w;
+  const float u1 = ((float)a + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+  const float u2 = (float)b * 2.3283064365386963e-10f;
+  const float rad = sqrtf(-2.0f * __logf(u1));
+  float s, c;
+  __sincosf(6.283185307179586f * u2, &s, &c);
+  return (lane & 1) ? rad * s : rad * c;
+}
+
+// Where a network row takes its inputs from (stream mode vs direct forward).
+struct RowSrc {
+  const int64_t* row_info;  // stream mode: ring bookkeeping; nullptr in direct mode
+  const double* ts;         // stream: row_t per ring row; direct: t per net row
+  int64_t R;                // ring rows (stream) / net rows (direct)
+  int cfg;                  // stream mode: net rows [0,R) uncond, [R,2R) cond
+  const double* emb;        // stream: [S, E]; direct: [rows, E]
+  const double* neg;        // stream + cfg: [S, E] or nullptr (zeros)
+  int E;
+};
+
+// ============================================================ K1: conditioning
+// c = MLP(sinusoid(1000 t)) + Linear(emb); out = bf16(SiLU(c)) (adaLN input)
+__global__ void cond_kernel(RowSrc src, int hidden, int freq_dim, const __nv_bfloat16* __restrict__ w1t,
+                            const float* __restrict__ b1, const __nv_bfloat16* __restrict__ w2t,
+                            const float* __restrict__ b2, const __nv_bfloat16* __restrict__ ywt,
+                            const float* __restrict__ yb, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float sh[];
+  float* f = sh;                // [freq_dim]
+  float* h1 = sh + freq_dim;    // [hidden]
+  float* e = h1 + hidden;       // [E]
+  const int64_t i = blockIdx.x;  // net row
+  const int64_t lr = i % src.R;
+  const double t = src.ts[lr];
+  const double* er;
+  bool zero_emb = false;
+  if (src.row_info) {
+    const int64_t s = src.row_info[lr * 4 + 3];
+    if (src.cfg && i < src.R) {
+      er = src.neg ? src.neg + s * src.E : nullptr;
+      zero_emb = src.neg == nullptr;
+    } else {
+      er = src.emb + s * src.E;
+    }
+  } else {
+    er = src.emb + i * src.E;
+  }
+  const int n = threadIdx.x;
+  const int half = freq_dim / 2;
+  const float tm = (float)(1000.0 * t);
+  for (int k = n; k < half; k += blockDim.x) {
+    const float fr = expf(-9.210340371976184f * (float)k / (float)half);  // ln(10000)
+    const float a = tm * fr;
+    f[k] = cosf(a);
+    f[half + k] = sinf(a);
+  }
+  for (int k = n; k < src.E; k += blockDim.x) e[k] = zero_emb ? 0.0f : (float)er[k];
+  __syncthreads();
+  if (n < hidden) {
+    float acc = b1[n];
+    for (int k = 0; k < freq_dim; ++k) acc += f[k] * __bfloat162float(w1t[(int64_t)k * hidden + n]);
+    h1[n] = silu(acc);
+  }
+  __syncthreads();
+  if (n < hidden) {
+    float acc = b2[n];
+    for (int k = 0; k < hidden; ++k) acc += h1[k] * __bfloat162float(w2t[(int64_t)k * hidden + n]);
+    float y = yb[n];
+    for (int k = 0; k < src.E; ++k) y += e[k] * __bfloat162float(ywt[(int64_t)k * hidden + n]);
+    out[i * hidden + n] = __float2bfloat16_rn(silu(acc + y));
+  }
+}
+
+// ============================================================ K2+K4: patch embed + pos + LN1 modulate
+// One warp per token; lane owns columns 128u + 4 lane + {0..3}, u < hidden/128.
+template <int HID>
+__global__ void patch_embed_ln_kernel(const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C,
+                                      const __nv_bfloat16* __restrict__ pw, const float* __restrict__ pb,
+                                      const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
+                                      float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod,
+                                      int64_t total_tokens) {
+  constexpr int U = HID / 128;
+  extern __shared__ float sw[];  // [HID][PK] fp32
+  const int PK = C * P * P;
+  for (int idx = threadIdx.x; idx < HID * PK; idx += blockDim.x) sw[idx] = __bfloat162float(pw[idx]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (tok >= total_tokens) return;
+  const int gw = HW / P, T = gw * gw;
+  const int64_t ni = tok / T;
+  const int tau = (int)(tok % T);
+  const int pi = tau / gw, pj = tau % gw;
+  const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
+  float v[16];
+  for (int c = 0; c < C; ++c)
+    for (int p = 0; p < P; ++p)
+      for (int q = 0; q < P; ++q) v[(c * P + p) * P + q] = xl[(int64_t)c * HW * HW + (pi * P + p) * HW + pj * P + q];
+  float y[U][4];
+  float sum = 0.f;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n0 = 128 * u + 4 * lane;
+    const float4 bb = *reinterpret_cast<const float4*>(pb + n0);
+    const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)tau * HID + n0);
+    float a[4] = {bb.x + pp.x, bb.y + pp.y, bb.z + pp.z, bb.w + pp.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float acc = 0.f;
+      for (int k = 0; k < PK; ++k) acc += v[k] * sw[(n0 + r) * PK + k];
+      const float val = __bfloat162float(__float2bfloat16_rn(acc + a[r]));  // residual stored bf16
+      y[u][r] = val;
+      sum += val;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / HID;
+  float var = 0.f;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+  const float rstd = rsqrtf(var / HID + ln_eps);
+  const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
+  const float* scale = shift + HID;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int n0 = 128 * u + 4 * lane;
+    const float4 sh = *reinterpret_cast<const float4*>(shift + n0);
+    const float4 sc = *reinterpret_cast<const float4*>(scale + n0);
+    const float shv[4] = {sh.x, sh.y, sh.z, sh.w}, scv[4] = {sc.x, sc.y, sc.z, sc.w};
+    float o[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) o[r] = (y[u][r] - mean) * rstd * (1.0f + scv[r]) + shv[r];
+    *reinterpret_cast<uint2*>(xres + tok * HID + n0) = make_uint2(pack_bf16(y[u][0], y[u][1]), pack_bf16(y[u][2], y[u][3]));
+    *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]));
+  }
+}
+
+// ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
+struct StepCoefF {
+  float lam, eta, span, dt;
+  bool at_end;
+};
+
+template <int HID, bool STREAM>
+__global__ void final_layer_kernel(const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw,
+                                   const float* __restrict__ fb, int HW, int P, int C, int64_t lat_rows,
+                                   // direct mode
+                                   float* __restrict__ eps_out,
+                                   // stream mode
+                                   const int64_t* __restrict__ ctl, int n, int64_t m, const double* __restrict__ stage_params,
+                                   const int64_t* __restrict__ row_info, int cfg, float w, float* __restrict__ x_ring,
+                                   const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
+                                   int64_t* __restrict__ frame_ids, int64_t total_tokens) {
+  constexpr int U = HID / 128;
+  const int PK = C * P * P;  // 16 outputs per token
+  extern __shared__ float sw[];  // [PK][HID] + bias[PK]
+  for (int idx = threadIdx.x; idx < PK * HID; idx += blockDim.x) sw[idx] = __bfloat162float(fw[idx]);
+  for (int idx = threadIdx.x; idx < PK; idx += blockDim.x) sw[PK * HID + idx] = fb[idx];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // over lat_rows * T
+  if (tok >= total_tokens) return;
+  const int gw = HW / P, T = gw * gw;
+  const int64_t lr = tok / T;
+  const int tau = (int)(tok % T);
+
+  auto project = [&](int64_t net_row, float (&eo)[16]) {
+    const __nv_bfloat16* xr = xmod + (net_row * T + tau) * HID;
+    float xv[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(xr + 128 * u + 4 * lane);
+      const float2 a = unpack_bf16(raw.x), b = unpack_bf16(raw.y);
+      xv[u][0] = a.x;
+      xv[u][1] = a.y;
+      xv[u][2] = b.x;
+      xv[u][3] = b.y;
+    }
+#pragma unroll
+    for (int f = 0; f < 16; ++f) {
+      float acc = 0.f;
+      if (f < PK) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc += xv[u][r] * sw[f * HID + 128 * u + 4 * lane + r];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      eo[f] = acc;
+    }
+  };
+
+  float ec[16];
+  project(STREAM && cfg ? lr + lat_rows : lr, ec);
+  float e = 0.f;
+#pragma unroll
+  for (int f = 0; f < 16; ++f)
+    if (lane == f) e = ec[f];
+  if (lane < PK) e += sw[PK * HID + lane];
+  if constexpr (STREAM) {
+    if (cfg) {
+      float eu_all[16];
+      project(lr, eu_all);
+      float eu = 0.f;
+#pragma unroll
+      for (int f = 0; f < 16; ++f)
+        if (lane == f) eu = eu_all[f];
+      if (lane < PK) eu += sw[PK * HID + lane];
+      e = __fadd_rn(eu, __fmul_rn(w, __fsub_rn(e, eu)));  // handle_cfg (models.py:288-293)
+    }
+  }
+  if (lane >= PK) return;
+  // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
+  const int c = lane % C, q = (lane / C) % P, p = lane / (C * P);
+  const int pi = tau / gw, pj = tau % gw;
+  const int64_t D = (int64_t)C * HW * HW;
+  const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
+  if constexpr (!STREAM) {
+    eps_out[lr * D + idx] = e;
+  } else {
+    const int64_t j = ctl[1];
+    const int64_t stage = row_info[lr * 4 + 0];
+    const int64_t g = row_info[lr * 4 + 1];
+    const bool active = row_info[lr * 4 + 2] != 0;
+    const int64_t s = row_info[lr * 4 + 3];
+    const int64_t k = lr % n;
+    const bool refill_slot = (k == (j + 1) % n);
+    const bool admit = refill_slot && (j + 1 < m);
+    const bool retiring = active && (stage + 1 == n);
+    if (refill_slot && tau == 0 && lane == 0) frame_ids[s] = retiring ? g : -1;
+    float* xr = x_ring + lr * D;
+    const float noise = admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx))
+                              : 0.0f;
+    if (active) {
+      const double* p = stage_params + stage * SF_PARAM_STRIDE;
+      const float lam = __double2float_rn(p[SF_P_LAMBDA_T]), eta = __double2float_rn(p[SF_P_ETA_T]);
+      const float span = __double2float_rn(p[SF_P_SPAN]), dt = __double2float_rn(p[SF_P_DT]);
+      const bool at_end = p[SF_P_AT_END] != 0.0;
+      const float x = xr[idx];
+      // velocity.py:125-130 in fp32
+      const float x_pred = __fadd_rn(__fmul_rn(lam, x), __fmul_rn(eta, e));
+      const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, x), span);
+      const float xn = __fadd_rn(x, __fmul_rn(dt, v));
+      if (retiring) frames_out[s * D + idx] = xn;
+      xr[idx] = admit ? noise : xn;
+    } else if (admit) {
+      xr[idx] = noise;
+    }
+  }
+}
+
+__global__ void stream_reset_f32_kernel(int64_t* ctl, int64_t S, int n, int64_t D, float* x_ring,
+                                        const float* noise0, uint64_t noise_seed) {
+  const int64_t s = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x)
+    x_ring[(s * n) * D + i] = noise0 ? noise0[s * D + i] : philox_normal(noise_seed + (uint64_t)s, 0, i);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    ctl[0] = 0;
+    ctl[1] = -1;
+  }
+}
+
+__global__ void philox_fill_kernel(float* out, int64_t S, int64_t D, uint64_t seed, int64_t gen) {
+  const int64_t s = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x)
+    out[s * D + i] = philox_normal(seed + (uint64_t)s, gen, i);
+}
+
+}  // namespace sf
+
+// ============================================================ handle
+using namespace sf;
+
+struct sf_dit {
+  sf_dit_config cfg;
+  sf_dit_weights w;
+  int64_t max_rows;
+  int tokens;
+  int64_t mod_stride;
+  // workspace carve-out
+  __nv_bfloat16 *cond, *xres, *xmod, *q, *k, *vt, *attn, *hmid;
+  float* mod;
+  // TMA descriptors
+  CUtensorMap a_cond, a_xmod, a_attn, a_hmid, b_ada;
+  std::vector<CUtensorMap> b_qkv, b_proj, b_fc1, b_fc2;
+  AttnMaps attn_maps;
+  std::map<std::tuple<const void*, int64_t, int, int64_t, double, const void*, const void*, const void*>,
+           cudaGraphExec_t>
+      graphs;
+};
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[9]*/) {
+  const int64_t T = (int64_t)(c.latent_hw / c.patch) * (c.latent_hw / c.patch);
+  const int64_t M = rows * T, H = c.hidden;
+  const int64_t mod_stride = (int64_t)c.depth * 6 * H + 2 * H;
+  const int64_t rows_pad = align_up(rows, 128);
+  int64_t o = 0;
+  auto take = [&](int i, int64_t bytes) {
+    off[i] = o;
+    o = align_up(o + bytes, 1024);
+  };
+  take(0, rows_pad * H * 2);          // cond (bf16 SiLU(c))
+  take(1, rows * mod_stride * 4);     // mod (fp32)
+  take(2, M * H * 2);                 // xres
+  take(3, M * H * 2);                 // xmod
+  take(4, M * H * 2);                 // q
+  take(5, M * H * 2);                 // k
+  take(6, M * H * 2);                 // vt
+  take(7, M * H * 2);                 // attn out
+  take(8, M * (int64_t)c.mlp_hidden * 2);  // mlp hidden
+  return o;
+}
+
+static int run_forward_core(sf_dit* h, int64_t rows, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const int H = c.hidden, T = h->tokens;
+  const int64_t M = rows * T;
+  int rc;
+  // adaLN for every block + final layer at once: mod[rows, mod_stride]
+  {
+    EpiParams ep{};
+    ep.bias = h->w.ada_b;
+    ep.out = h->mod;
+    ep.ldo = h->mod_stride;
+    ep.tokens_per_slot = 1 << 30;
+    ep.M = (int)rows;
+    if ((rc = launch_gemm(EPI_F32, 256, h->a_cond, h->b_ada, (int)rows, (int)h->mod_stride, H, ep, st))) return rc;
+  }
+  return SF_OK;
+}
+
+static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const int H = c.hidden, T = h->tokens;
+  const int64_t M = rows * T;
+  const int64_t B6 = 6 * (int64_t)H;
+  int rc;
+  for (int l = 0; l < c.depth; ++l) {
+    {
+      EpiParams ep{};
+      ep.bias = h->w.qkv_b + (int64_t)l * 3 * H;
+      ep.q = h->q;
+      ep.k = h->k;
+      ep.vt = h->vt;
+      ep.heads = c.heads;
+      ep.q_scale = 0.125f;  // 1/sqrt(64)
+      ep.tokens_per_slot = T;
+      ep.M = (int)M;
+      if ((rc = launch_gemm(EPI_QKV, 192, h->a_xmod, h->b_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+    }
+    if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
+    {
+      EpiParams ep{};
+      ep.bias = h->w.proj_b + (int64_t)l * H;
+      ep.xres = h->xres;
+      ep.xmod = h->xmod;
+      ep.gate = h->mod + l * B6 + 2 * H;   // gate_msa
+      ep.shift = h->mod + l * B6 + 3 * H;  // shift_mlp
+      ep.scale = h->mod + l * B6 + 4 * H;  // scale_mlp
+      ep.vec_stride = h->mod_stride;
+      ep.ln_eps = c.ln_eps;
+      ep.tokens_per_slot = T;
+      ep.M = (int)M;
+      if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_attn, h->b_proj[l], (int)M, H, H, ep, st))) return rc;
+    }
+    {
+      EpiParams ep{};
+      ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
+      ep.out = h->hmid;
+      ep.ldo = c.mlp_hidden;
+      ep.tokens_per_slot = T;
+      ep.M = (int)M;
+      if ((rc = launch_gemm(EPI_GELU, 256, h->a_xmod, h->b_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
+    }
+    {
+      EpiParams ep{};
+      ep.bias = h->w.fc2_b + (int64_t)l * H;
+      ep.xres = h->xres;
+      ep.xmod = h->xmod;
+      ep.gate = h->mod + l * B6 + 5 * H;  // gate_mlp
+      const float* nxt = (l + 1 < c.depth) ? h->mod + (l + 1) * B6  // next block: shift_msa, scale_msa
+                                           : h->mod + c.depth * B6;  // final layer: shift, scale
+      ep.shift = nxt;
+      ep.scale = nxt + H;
+      ep.vec_stride = h->mod_stride;
+      ep.ln_eps = c.ln_eps;
+      ep.tokens_per_slot = T;
+      ep.M = (int)M;
+      if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_hmid, h->b_fc2[l], (int)M, H, c.mlp_hidden, ep, st))) return rc;
+    }
+  }
+  return SF_OK;
+}
+
+static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const size_t sm = (c.freq_dim + c.hidden + c.embed_dim) * sizeof(float);
+  cond_kernel<<<(unsigned)rows, c.hidden, sm, st>>>(src, c.hidden, c.freq_dim, (const __nv_bfloat16*)h->w.t_w1t,
+                                                     h->w.t_b1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2,
+                                                     (const __nv_bfloat16*)h->w.y_wt, h->w.y_b, h->cond);
+  return cuda_status();
+}
+
+static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t rows, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const int64_t tokens = rows * h->tokens;
+  const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
+  const unsigned blocks = (unsigned)((tokens + 7) / 8);
+  patch_embed_ln_kernel<384><<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch,
+                                                      (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b,
+                                                      h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres,
+                                                      h->xmod, tokens);
+  return cuda_status();
+}
+
+static size_t final_smem(const sf_dit_config& c) {
+  const int PK = c.in_ch * c.patch * c.patch;
+  return (size_t)(PK * c.hidden + PK) * sizeof(float);
+}
+
+extern "C" {
+
+int64_t sf_dit_workspace_bytes(const sf_dit_config* cfg, int64_t max_rows) {
+  int64_t off[9];
+  return ws_layout(*cfg, max_rows, off);
+}
+
+int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max_rows, void* workspace,
+                  int64_t ws_bytes, sf_dit** out) {
+  if (!cfg || !w || !out || max_rows < 1) return SF_ERR_PARAMETER;
+  const sf_dit_config& c = *cfg;
+  if (c.hidden != 384 || c.heads * 64 != c.hidden || c.patch != 2 || c.in_ch != 4 || c.latent_hw % 32 ||
+      c.mlp_hidden != 4 * c.hidden || c.freq_dim % 2 || c.embed_dim < 1 || c.embed_dim > 64)
+    return SF_ERR_PARAMETER;  // this build's kernels are specialised for hidden 384 / head dim 64 / patch 2
+  int64_t off[9];
+  if (ws_layout(c, max_rows, off) > ws_bytes) return SF_ERR_PARAMETER;
+  auto* h = new sf_dit();
+  h->cfg = c;
+  h->w = *w;
+  h->max_rows = max_rows;
+  const int gw = c.latent_hw / c.patch;
+  h->tokens = gw * gw;
+  const int H = c.hidden;
+  h->mod_stride = (int64_t)c.depth * 6 * H + 2 * H;
+  uint8_t* base = (uint8_t*)workspace;
+  h->cond = (__nv_bfloat16*)(base + off[0]);
+  h->mod = (float*)(base + off[1]);
+  h->xres = (__nv_bfloat16*)(base + off[2]);
+  h->xmod = (__nv_bfloat16*)(base + off[3]);
+  h->q = (__nv_bfloat16*)(base + off[4]);
+  h->k = (__nv_bfloat16*)(base + off[5]);
+  h->vt = (__nv_bfloat16*)(base + off[6]);
+  h->attn = (__nv_bfloat16*)(base + off[7]);
+  h->hmid = (__nv_bfloat16*)(base + off[8]);
+  const int64_t M = max_rows * h->tokens;
+  const int64_t rows_pad = align_up(max_rows, 128);
+  int rc = SF_OK;
+  rc |= make_tmap_bf16_2d(&h->a_cond, h->cond, H, rows_pad, H, 64, 128);
+  rc |= make_tmap_bf16_2d(&h->a_xmod, h->xmod, H, M, H, 64, 128);
+  rc |= make_tmap_bf16_2d(&h->a_attn, h->attn, H, M, H, 64, 128);
+  rc |= make_tmap_bf16_2d(&h->a_hmid, h->hmid, c.mlp_hidden, M, c.mlp_hidden, 64, 128);
+  rc |= make_tmap_bf16_2d(&h->b_ada, w->ada_w, H, h->mod_stride, H, 64, gemm_b_box_rows(256));
+  h->b_qkv.resize(c.depth);
+  h->b_proj.resize(c.depth);
+  h->b_fc1.resize(c.depth);
+  h->b_fc2.resize(c.depth);
+  for (int l = 0; l < c.depth; ++l) {
+    const __nv_bfloat16* qkv = (const __nv_bfloat16*)w->qkv_w + (int64_t)l * 3 * H * H;
+    const __nv_bfloat16* proj = (const __nv_bfloat16*)w->proj_w + (int64_t)l * H * H;
+    const __nv_bfloat16* fc1 = (const __nv_bfloat16*)w->fc1_w + (int64_t)l * c.mlp_hidden * H;
+    const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
+    rc |= make_tmap_bf16_2d(&h->b_qkv[l], qkv, H, 3 * H, H, 64, gemm_b_box_rows(192));
+    rc |= make_tmap_bf16_2d(&h->b_proj[l], proj, H, H, H, 64, gemm_b_box_rows(384));
+    rc |= make_tmap_bf16_2d(&h->b_fc1[l], fc1, H, c.mlp_hidden, H, 64, gemm_b_box_rows(256));
+    rc |= make_tmap_bf16_2d(&h->b_fc2[l], fc2, c.mlp_hidden, H, c.mlp_hidden, 64, gemm_b_box_rows(384));
+  }
+  rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
+  if (rc != SF_OK) {
+    delete h;
+    return SF_ERR_CUDA;
+  }
+  // kernel attributes (dynamic smem > 48 KB) set once, outside any graph capture
+  cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)));
+  cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)final_smem(c));
+  cudaFuncSetAttribute(final_layer_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)final_smem(c));
+  *out = h;
+  return cuda_status();
+}
+
+int sf_dit_destroy(sf_dit* h) {
+  if (!h) return SF_OK;
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  delete h;
+  return SF_OK;
+}
+
+int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, const double* row_embs, float* eps_out,
+                   void* stream) {
+  if (!h || rows < 1 || rows > h->max_rows) return SF_ERR_PARAMETER;
+  cudaStream_t st = (cudaStream_t)stream;
+  const sf_dit_config& c = h->cfg;
+  RowSrc src{nullptr, ts, rows, 0, row_embs, nullptr, c.embed_dim};
+  int rc;
+  if ((rc = launch_cond(h, src, rows, st))) return rc;
+  if ((rc = run_forward_core(h, rows, st))) return rc;
+  if ((rc = launch_patch(h, x, rows, rows, st))) return rc;
+  if ((rc = run_blocks(h, rows, st))) return rc;
+  const int64_t tokens = rows * h->tokens;
+  final_layer_kernel<384, false><<<(unsigned)((tokens + 7) / 8), 256, final_smem(c), st>>>(
+      h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, rows, eps_out,
+      nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr, tokens);
+  return cuda_status();
+}
+
+static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
+                                int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
+                                double w, const float* noise_in, uint64_t noise_seed, float* frames_out,
+                                int64_t* frame_ids, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const int64_t R = S * n;
+  const int cfg = (w != 1.0) ? 1 : 0;
+  const int64_t rows = cfg ? 2 * R : R;
+  int rc;
+  if ((rc = sf_stream_prepare(ctl, S, n, m, stage_params, row_info, row_t, st))) return rc;
+  RowSrc src{row_info, row_t, R, cfg, emb, neg, c.embed_dim};
+  if ((rc = launch_cond(h, src, rows, st))) return rc;
+  if ((rc = run_forward_core(h, rows, st))) return rc;
+  if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;
+  if ((rc = run_blocks(h, rows, st))) return rc;
+  const int64_t tokens = R * h->tokens;
+  final_layer_kernel<384, true><<<(unsigned)((tokens + 7) / 8), 256, final_smem(c), st>>>(
+      h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
+      m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
+  return cuda_status();
+}
+
+int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
+                       int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
+                       const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                       int32_t use_graph, void* stream) {
+  if (!h || S < 1 || n < 1 || m < 1) return SF_ERR_PARAMETER;
+  const int64_t rows = (w != 1.0 ? 2 : 1) * S * n;
+  if (rows > h->max_rows) return SF_ERR_PARAMETER;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!use_graph)
+    return stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+                                noise_seed, frames_out, frame_ids, st);
+  auto key = std::make_tuple((const void*)x_ring, S, n, m, w, (const void*)noise_in, (const void*)frames_out,
+                             (const void*)ctl);
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    cudaGraph_t g;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return SF_ERR_CUDA;
+    int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+                                  noise_seed, frames_out, frame_ids, st);
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (rc != SF_OK || e != cudaSuccess) return rc != SF_OK ? rc : SF_ERR_CUDA;
+    cudaGraphExec_t ge;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return SF_ERR_CUDA;
+    it = h->graphs.emplace(key, ge).first;
+  }
+  return cudaGraphLaunch(it->second, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+}
+
+int sf_dit_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, float* x_ring, const float* noise0,
+                        uint64_t noise_seed, void* stream) {
+  if (S < 1 || n < 1 || D < 1 || S > 65535) return SF_ERR_PARAMETER;
+  dim3 grid(16, (unsigned)S);
+  stream_reset_f32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ctl, S, n, D, x_ring, noise0, noise_seed);
+  return cuda_status();
+}
+
+int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t gen, void* stream) {
+  if (S < 1 || D < 1 || S > 65535) return SF_ERR_PARAMETER;
+  dim3 grid(16, (unsigned)S);
+  philox_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out, S, D, seed, gen);
+  return cuda_status();
+}
+
+int sf_dit_mod_stride(const sf_dit_config* c) { return c->depth * 6 * c->hidden + 2 * c->hidden; }
+
+}  // extern "C"

@@ -1,6 +1,7 @@
 // Internal declarations shared by the .cu translation units.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/streamflow.h"
@@ -12,6 +13,12 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 int gemm_b_box_rows(int bn);
 int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                 const EpiParams& ep, cudaStream_t st);
+
+struct AttnMaps {
+  CUtensorMap q, k, v;
+};
+int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T);
+int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st);
 
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
 }  // namespace sf
