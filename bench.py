@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark: frames/s of the 4-step heterogeneous-timestep stream batch with a
+random-init DiT-S/2 velocity field on a 64x64x4 latent (512^2 image), bf16
+network / fp32 latent state, on B200 (BASELINE.json configs[1]; streams
+partitioned across GPUs, configs[4]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--streams S] [--impl ours|reference]
+
+One "step" = one stream-batch iteration: every in-flight slot of every stream
+gets one velocity evaluation + fused Euler update; after warm-up exactly one
+frame per stream retires per step.  ``value`` counts frames/s over all GPUs
+with inputs resident in HBM (on-device Philox admission noise, CUDA-graph
+replay); ``e2e`` repeats the measurement through the public StreamBatch API
+with HOST buffers (H2D of each step's admission noise from pinned memory, D2H
+of the emitted frames, both inside the timed region).
+
+``--impl reference`` times the reference's CPU implementation of the same path
+(the oracle port: oracle/flowpipe_oracle.py + oracle/dit_oracle.py, torch fp32
+on all host threads) on a bounded sample (one stream per step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 512² latent, 4-step stream batch; p50 per-frame latency ms"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=32, help="streams per GPU")
+    ap.add_argument("--n", type=int, default=4, help="steps per generation (slots per stream)")
+    ap.add_argument("--windows", type=int, default=4, help="time windows K of the scheduler")
+    ap.add_argument("--guidance", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(args, world):
+    return {
+        "workload": "DiT-S/2 random-init velocity field, 64x64x4 latent (512^2), "
+                    f"{args.n}-step heterogeneous stream batch, {args.streams} streams/GPU x {args.n} slots",
+        "model": "DiT-S/2 (depth 12, hidden 384, 6 heads, patch 2, 1024 tokens)",
+        "streams_per_gpu": args.streams,
+        "streams_total": args.streams * world,
+        "slots_per_gpu": args.streams * args.n,
+        "steps_per_generation": args.n,
+        "time_windows": args.windows,
+        "guidance_scale": args.guidance,
+        "global_batch": args.streams * args.n * world * (2 if args.guidance != 1.0 else 1),
+        "seq_len": 1024,
+        "parallelism": f"stream-partitioned x{world} (no collective in the step)",
+        "l2": "activation working set per step > 126 MB L2 (no flush needed)",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import torch
+
+    from oracle.cpu_bench import CpuStream
+    from paper_2511_22009_b200.dit import DIT_S2, init_dit_params
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    params = init_dit_params(DIT_S2, seed=0)
+    cs = CpuStream(params, DIT_S2.heads, n=args.n, num_windows=args.windows, w=args.guidance, seed=1000)
+    for _ in range(args.warmup):
+        cs.iteration()
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cs.iteration()
+        times.append(time.perf_counter() - t0)
+    total = time.perf_counter() - t_all
+    value = args.steps / total  # one frame retires per iteration of one stream
+    lat = [1e3 * sum(times[i:i + args.n]) for i in range(max(1, len(times) - args.n + 1))]
+    sample = (f"1 stream x {args.n} slots per step (steady state), DiT-S/2 torch fp32 CPU oracle port, "
+              f"{args.steps} steps; streams are independent so frames/s scales per stream")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (N(0,1) latents, random-init weights)",
+        "config": workload(args, 1), "p50_latency_ms": statistics.median(lat),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    args.warmup = max(args.warmup, 3, args.n)
+    rank, world, local = env_rank()
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_22009_b200.build import build
+
+    build()
+    import paper_2511_22009_b200 as sf
+    from paper_2511_22009_b200.dit import DIT_S2
+
+    cfg = DIT_S2
+    S, n, w = args.streams, args.n, args.guidance
+    rows = S * n * (2 if w != 1.0 else 1)
+    model = sf.DiTVelocityModel(cfg, seed=0, max_rows=rows)
+    sched = sf.build_time_window_schedule(num_windows=args.windows, inference_steps=n)
+    seeds = [1000 + rank * S + s for s in range(S)]
+    conds = [sf.make_conditioning(np.random.default_rng([sd, 2**32 - 1]).standard_normal(cfg.embed_dim),
+                                  guidance_scale=w) for sd in seeds]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, dtype=np.float32, noise="device")
+    for _ in range(args.warmup):
+        sb.launch()
+    torch.cuda.synchronize()
+
+    def timed(step_fn, K):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(K):
+            step_fn()
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        steps = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
+        total = ev[0].elapsed_time(ev[K])
+        if world > 1:
+            t = torch.tensor([total], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return total, steps
+
+    clocks = Clocks(local)
+    total_ms, step_ms = timed(sb.launch, args.steps)
+    clk = clocks.stop()
+    frames = world * S * args.steps
+    value = frames / (total_ms / 1e3)
+    lat = [sum(step_ms[i:i + n]) for i in range(max(1, len(step_ms) - n + 1))]
+    p50 = statistics.median(lat)
+    p99 = float(np.percentile(lat, 99))
+
+    # ---- end to end through the public API with host buffers
+    sb_e2e = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, dtype=np.float32, noise="host")
+    g = torch.Generator().manual_seed(rank)
+    pool = [torch.randn(S, cfg.dim, generator=g).pin_memory() for _ in range(4)]
+    fdst = torch.empty(S, cfg.dim, dtype=torch.float32).pin_memory()
+    it = {"i": 0}
+
+    def e2e_step():
+        it["i"] += 1
+        sb_e2e.launch_host_io(pool[it["i"] % len(pool)], fdst)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms, _ = timed(e2e_step, args.steps)
+    e2e_value = frames / (e2e_ms / 1e3)
+
+    # ---- per-kernel roofline from a profiled eager step (CUDA events per launch)
+    sb.profile_step()
+    prof = sb.profile_step()
+    T, H, Fm, L = cfg.tokens, cfg.hidden, cfg.mlp_hidden, cfg.depth
+    M = rows * T
+    flops = {
+        "qkv_gemm": L * 2.0 * M * 3 * H * H, "attention": L * 4.0 * rows * T * T * H,
+        "proj_gemm_res_ln": L * 2.0 * M * H * H, "fc1_gemm_gelu": L * 2.0 * M * Fm * H,
+        "fc2_gemm_res_ln": L * 2.0 * M * H * Fm, "adaln_gemm": 2.0 * rows * (6 * H * L + 2 * H) * H,
+    }
+    burst, sustained, hbm, src = peaks()
+    dom = max(flops, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    achieved = flops[dom] / (dom_ms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)
+    except Exception:
+        pass
+    launches_per_step = sum(c for _, c in prof.values())
+    step_flops = rows * cfg.flops_per_row()
+    per_kernel = {k: {"ms_per_step": round(v[0], 4), "launches": v[1],
+                      **({"tflops": round(flops[k] / (v[0] / 1e3) / 1e12, 1)} if k in flops and v[0] > 0 else {})}
+                  for k, v in prof.items()}
+
+    # ---- stream-partitioned output: NCCL gather of the last frames + frame counts (off the timed region)
+    gathered = None
+    if world > 1:
+        out = torch.empty(world * S, cfg.dim, device="cuda")
+        dist.all_gather_into_tensor(out, sb.frames.contiguous())
+        cnt = torch.tensor([float(frames / world)], device="cuda")
+        dist.all_reduce(cnt)
+        gathered = {"frames_gathered_rank0": int(out.shape[0]), "frames_total": int(cnt.item())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.cpu_bench import cpu_stream_throughput
+
+        r = cpu_stream_throughput(model.params, cfg.heads, iters=2, warmup=1, n=n, num_windows=args.windows,
+                                  w=w, seed=1000)
+        cpu = {"value": r["frames_per_s"], "unit": "frames/s", "cores": r["threads"], "kind": "port",
+               "sample": f"1 stream x {n} slots, 2 timed steady-state iterations (+1 warm-up) of the torch-fp32 "
+                         "DiT-S/2 oracle port + numpy Euler step"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (N(0,1) latents from on-device Philox, random-init DiT-S/2 weights)",
+            "config": workload(args, world),
+            "p50_latency_ms": p50, "p99_latency_ms": p99,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": S * cfg.dim * 4,
+                    "d2h_bytes_per_step": S * cfg.dim * 4},
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 1),
+                         "peak": burst, "unit": "TFLOP/s", "frac": round(achieved / burst, 4),
+                         "traffic": traffic, "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
+                         "flops_per_launch": flops[dom] / max(dom_n, 1), "launches_per_step": dom_n},
+            "step_roofline": {"achieved_tflops": round(step_flops / (total_ms / args.steps / 1e3) / 1e12, 1),
+                              "peak": sustained, "frac": round(step_flops / (total_ms / args.steps / 1e3) / 1e12
+                                                               / sustained, 4),
+                              "flops_per_step": step_flops, "peak_source": f"{src} bf16 sustained"},
+            "kernels": per_kernel,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        if gathered:
+            line["gather"] = gathered
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

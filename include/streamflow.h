@@ -224,6 +224,19 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
                        const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
                        int32_t use_graph, void* stream);
 
+/* One eager (non-graph) stream step with a CUDA event after every launch;
+ * synchronises and returns, per kernel class, the summed duration (ms) and the
+ * launch count.  Classes: 0 prepare, 1 cond, 2 adaLN GEMM, 3 patch-embed+LN,
+ * 4 QKV GEMM, 5 attention, 6 proj GEMM+res+LN, 7 fc1 GEMM+GELU,
+ * 8 fc2 GEMM+res+LN, 9 final+CFG+Euler+refill (arrays of >= 10 entries). */
+int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
+                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
+                        double w, const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                        float* ms_per_class, int32_t* launches_per_class, void* stream);
+
+/* Number of kernel launches this handle has issued or captured so far. */
+int64_t sf_dit_launch_count(const sf_dit* h);
+
 /* Reset a fp32 ring: generation-0 noise into slot 0 of each stream (noise0 [S, D]
  * or Philox when NULL), ctl <- j = 0. */
 int sf_dit_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, float* x_ring, const float* noise0,

@@ -257,7 +257,7 @@ int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, in
   return SF_OK;
 }
 
-int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st) {
+int prepare_attn_kernel() {
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attn_fwd_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::SMEM) !=
@@ -265,6 +265,11 @@ int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, 
       return SF_ERR_CUDA;
     attr = true;
   }
+  return SF_OK;
+}
+
+int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st) {
+  if (prepare_attn_kernel() != SF_OK) return SF_ERR_CUDA;
   dim3 grid(T / attn::BQ, (unsigned)(rows * heads));
   attn_fwd_tcgen05<<<grid, 192, attn::SMEM, st>>>(m.q, m.k, m.v, out, T, heads);
   return cuda_status();

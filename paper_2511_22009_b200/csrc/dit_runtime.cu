@@ -332,6 +332,12 @@ struct sf_dit {
   std::map<std::tuple<const void*, int64_t, int, int64_t, double, const void*, const void*, const void*>,
            cudaGraphExec_t>
       graphs;
+  cudaStream_t cap_stream = nullptr;
+  // profiling / accounting
+  int64_t launch_count = 0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_events;
+  std::vector<int> prof_cls;
 };
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -358,6 +364,21 @@ static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[9
   return o;
 }
 
+// Kernel classes for per-launch profiling (sf_dit_profile_step).
+enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_NCLS };
+
+// Called after every launch: counts launches and, in a profiled step, records
+// a CUDA event so each launch's duration can be attributed to its class.
+static void mark(sf_dit* h, int cls, cudaStream_t st) {
+  h->launch_count++;
+  if (!h->profiling) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  h->prof_events.push_back(e);
+  h->prof_cls.push_back(cls);
+}
+
 static int run_forward_core(sf_dit* h, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const int H = c.hidden, T = h->tokens;
@@ -372,6 +393,7 @@ static int run_forward_core(sf_dit* h, int64_t rows, cudaStream_t st) {
     ep.tokens_per_slot = 1 << 30;
     ep.M = (int)rows;
     if ((rc = launch_gemm(EPI_F32, 256, h->a_cond, h->b_ada, (int)rows, (int)h->mod_stride, H, ep, st))) return rc;
+    mark(h, P_ADALN, st);
   }
   return SF_OK;
 }
@@ -394,8 +416,10 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if ((rc = launch_gemm(EPI_QKV, 192, h->a_xmod, h->b_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+      mark(h, P_QKV, st);
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
+    mark(h, P_ATTN, st);
     {
       EpiParams ep{};
       ep.bias = h->w.proj_b + (int64_t)l * H;
@@ -409,6 +433,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_attn, h->b_proj[l], (int)M, H, H, ep, st))) return rc;
+      mark(h, P_PROJ, st);
     }
     {
       EpiParams ep{};
@@ -418,6 +443,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if ((rc = launch_gemm(EPI_GELU, 256, h->a_xmod, h->b_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
+      mark(h, P_FC1, st);
     }
     {
       EpiParams ep{};
@@ -434,6 +460,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_hmid, h->b_fc2[l], (int)M, H, c.mlp_hidden, ep, st))) return rc;
+      mark(h, P_FC2, st);
     }
   }
   return SF_OK;
@@ -445,6 +472,7 @@ static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t 
   cond_kernel<<<(unsigned)rows, c.hidden, sm, st>>>(src, c.hidden, c.freq_dim, (const __nv_bfloat16*)h->w.t_w1t,
                                                      h->w.t_b1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2,
                                                      (const __nv_bfloat16*)h->w.y_wt, h->w.y_b, h->cond);
+  mark(h, P_COND, st);
   return cuda_status();
 }
 
@@ -457,6 +485,7 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
                                                       (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b,
                                                       h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres,
                                                       h->xmod, tokens);
+  mark(h, P_PATCH, st);
   return cuda_status();
 }
 
@@ -527,6 +556,10 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     return SF_ERR_CUDA;
   }
   // kernel attributes (dynamic smem > 48 KB) set once, outside any graph capture
+  if (prepare_gemm_kernels() != SF_OK || prepare_attn_kernel() != SF_OK) {
+    delete h;
+    return SF_ERR_CUDA;
+  }
   cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)));
   cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -540,6 +573,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
 int sf_dit_destroy(sf_dit* h) {
   if (!h) return SF_OK;
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
   return SF_OK;
 }
@@ -572,6 +606,7 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   const int64_t rows = cfg ? 2 * R : R;
   int rc;
   if ((rc = sf_stream_prepare(ctl, S, n, m, stage_params, row_info, row_t, st))) return rc;
+  mark(h, P_PREPARE, st);
   RowSrc src{row_info, row_t, R, cfg, emb, neg, c.embed_dim};
   if ((rc = launch_cond(h, src, rows, st))) return rc;
   if ((rc = run_forward_core(h, rows, st))) return rc;
@@ -581,8 +616,48 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   final_layer_kernel<384, true><<<(unsigned)((tokens + 7) / 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
       m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
+  mark(h, P_FINAL, st);
   return cuda_status();
 }
+
+int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
+                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
+                        double w, const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                        float* ms_per_class, int32_t* launches_per_class, void* stream) {
+  if (!h || S < 1 || n < 1 || m < 1 || !ms_per_class || !launches_per_class) return SF_ERR_PARAMETER;
+  const int64_t rows = (w != 1.0 ? 2 : 1) * S * n;
+  if (rows > h->max_rows) return SF_ERR_PARAMETER;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->profiling = true;
+  h->prof_events.clear();
+  h->prof_cls.clear();
+  cudaEvent_t start;
+  cudaEventCreate(&start);
+  cudaEventRecord(start, st);
+  int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+                                noise_seed, frames_out, frame_ids, st);
+  h->profiling = false;
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = SF_ERR_CUDA;
+  for (int c = 0; c < P_NCLS; ++c) {
+    ms_per_class[c] = 0.f;
+    launches_per_class[c] = 0;
+  }
+  cudaEvent_t prev = start;
+  for (size_t i = 0; i < h->prof_events.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, prev, h->prof_events[i]);
+    ms_per_class[h->prof_cls[i]] += ms;
+    launches_per_class[h->prof_cls[i]] += 1;
+    prev = h->prof_events[i];
+  }
+  for (auto e : h->prof_events) cudaEventDestroy(e);
+  cudaEventDestroy(start);
+  h->prof_events.clear();
+  h->prof_cls.clear();
+  return rc;
+}
+
+int64_t sf_dit_launch_count(const sf_dit* h) { return h ? h->launch_count : -1; }
 
 int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
@@ -599,11 +674,15 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
                              (const void*)ctl);
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
+    // Capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on the caller's.
+    if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return SF_ERR_CUDA;
     cudaGraph_t g;
-    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return SF_ERR_CUDA;
+    if (cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return SF_ERR_CUDA;
     int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
-                                  noise_seed, frames_out, frame_ids, st);
-    cudaError_t e = cudaStreamEndCapture(st, &g);
+                                  noise_seed, frames_out, frame_ids, h->cap_stream);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc != SF_OK || e != cudaSuccess) return rc != SF_OK ? rc : SF_ERR_CUDA;
     cudaGraphExec_t ge;
     e = cudaGraphInstantiate(&ge, g, 0);

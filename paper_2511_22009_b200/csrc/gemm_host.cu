@@ -38,16 +38,36 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 }
 
 template <int BN, int KIND>
+static int set_attr() {
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GemmCfg<BN>::SMEM_BYTES) != cudaSuccess)
+      return SF_ERR_CUDA;
+    done = true;
+  }
+  return SF_OK;
+}
+
+// Set every instantiation's smem attribute up front (never inside a graph capture).
+int prepare_gemm_kernels() {
+  int rc = SF_OK;
+  rc |= set_attr<128, EPI_F32>();
+  rc |= set_attr<128, EPI_BF16>();
+  rc |= set_attr<128, EPI_GELU>();
+  rc |= set_attr<256, EPI_F32>();
+  rc |= set_attr<256, EPI_BF16>();
+  rc |= set_attr<256, EPI_GELU>();
+  rc |= set_attr<192, EPI_QKV>();
+  rc |= set_attr<384, EPI_RES_LN>();
+  return rc;
+}
+
+template <int BN, int KIND>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, const EpiParams& ep,
                       cudaStream_t st) {
   using C = GemmCfg<BN>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM_BYTES) != cudaSuccess)
-      return SF_ERR_CUDA;
-    attr_done = true;
-  }
+  if (set_attr<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
   dim3 grid(N / BN, (M + C::BM - 1) / C::BM);
   gemm_bf16_tcgen05<BN, KIND><<<grid, 192, C::SMEM_BYTES, st>>>(a, b, K, ep);
   return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA;

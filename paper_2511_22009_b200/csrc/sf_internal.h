@@ -11,6 +11,8 @@ struct EpiParams;
 int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
                       uint32_t box_inner, uint32_t box_outer);
 int gemm_b_box_rows(int bn);
+int prepare_gemm_kernels();
+int prepare_attn_kernel();
 int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                 const EpiParams& ep, cudaStream_t st);
 

@@ -144,7 +144,15 @@ _lib.SIGNATURES.update({
     "sf_dit_stream_reset": [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                             C.c_uint64, C.c_void_p],
     "sf_philox_normal": [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p],
+    "sf_dit_profile_step": [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                            C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+    "sf_dit_launch_count": [C.c_void_p],
 })
+_lib.RESTYPES["sf_dit_launch_count"] = C.c_int64
+
+PROFILE_CLASSES = ("prepare", "cond", "adaln_gemm", "patch_embed_ln", "qkv_gemm", "attention",
+                   "proj_gemm_res_ln", "fc1_gemm_gelu", "fc2_gemm_res_ln", "final_euler_refill")
 
 
 class DeviceDiT:

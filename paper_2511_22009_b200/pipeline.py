@@ -1,0 +1,428 @@
+"""Stream batch (Alg. 2) with a device-resident ring buffer.
+
+Drop-in for flowpipe pipeline.py:139-266 (``run_stream``, ``run_vanilla`` and
+their result / stats types) plus the device-resident ``StreamBatch`` the
+north star asks for: S independent streams x n in-flight slots, advanced in
+lockstep, one velocity evaluation per iteration for every slot.
+
+Ring layout: row r = s*n + k holds generation g of stream s
+with g = k (mod n); at iteration j its stage is (j - k) mod n and it is active
+iff 0 <= g < m.  The reference's ``buffer.insert(0, ...)`` / ``pop()`` shift is
+the implicit advance of j -- nothing moves in memory; the slot that retires
+generation j-n+1 is refilled in the same kernel with the noise of generation
+j+1.  Everything between ``step()`` calls stays on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ParameterError, StateError
+from .models import (Conditioning, DiTVelocityModel, SeededMockModel, VelocityModel, apply_cfg, busy_wait_us,
+                     handle_cfg)
+from .schedule import DeviceSchedule, TimeWindowSchedule
+from .velocity import LatentBatch, StepStats, batched_velocity_step, sequential_velocity_step, velocity_step_device
+
+
+# ----------------------------------------------------------------------------- reference result / stats types
+@dataclass
+class BufferEntry:
+    """pipeline.py:31-37."""
+
+    latent: np.ndarray
+    gen_id: int
+    stage: int
+
+
+@dataclass
+class PipelineState:
+    """Newest-first snapshot (pipeline.py:40-50)."""
+
+    buffer: list
+    stage_times: np.ndarray
+    emitted: int
+    iteration: int
+
+
+@dataclass(frozen=True)
+class DecodedPayload:
+    latent: np.ndarray
+
+
+@dataclass(frozen=True)
+class GenerationResult:
+    id: int
+    latent: np.ndarray
+    decoded: DecodedPayload
+    iterations_spanned: int
+
+
+@dataclass
+class RunStats:
+    """pipeline.py:68-83."""
+
+    model_calls: int = 0
+    scheduler_calls: int = 0
+    decodes: int = 0
+    decode_time_us: float = 0.0
+    step_stats: StepStats = field(default_factory=StepStats)
+
+    def merge(self, other: "RunStats") -> None:
+        self.model_calls += other.model_calls
+        self.scheduler_calls += other.scheduler_calls
+        self.decodes += other.decodes
+        self.decode_time_us += other.decode_time_us
+        self.step_stats.merge(other.step_stats)
+
+
+def decode_stub(latent, cost_us: float = 0.0) -> DecodedPayload:
+    """Identity decode with injected cost (pipeline.py:86-89)."""
+    busy_wait_us(cost_us)
+    return DecodedPayload(latent=np.array(latent, copy=True))
+
+
+def generation_noise(seed: int, gen_id: int, dim: int) -> np.ndarray:
+    """Initial noise of one generation (pipeline.py:92-98): numpy PCG64 seeded
+    by [seed, id].  This is the *input* of a generation; the device ring ingests
+    it (parity mode) or replaces it with on-device Philox (throughput mode)."""
+    return np.random.default_rng([seed, gen_id]).standard_normal(dim)
+
+
+def _check_run_args(m: int, n: int, sched: TimeWindowSchedule) -> None:
+    if m < 1:
+        raise ParameterError(f"need at least one generation, got m={m}")
+    if n < 1:
+        raise ParameterError(f"need at least one denoising step, got n={n}")
+    if sched.num_steps < n:
+        raise ParameterError(f"inference grid has {sched.num_steps} points, fewer than n={n} steps")
+
+
+_UNBOUNDED = 1 << 62
+
+
+class StreamBatch:
+    """Device-resident heterogeneous-timestep stream batch.
+
+    model      SeededMockModel / DiTVelocityModel (fused native step) or any
+               VelocityModel (generic path: model.forward + device Euler)
+    sched      TimeWindowSchedule (reference scheduler / time-grid arguments)
+    n          steps per generation (= in-flight slots per stream)
+    num_streams S independent streams (own seed and conditioning each)
+    cond       one Conditioning for all streams or a list of S
+    seed       run seed of stream 0 (stream s uses seed + s) or a list of S
+    m          generations per stream (None = unbounded serving)
+    dtype      latent dtype (np.float64 / np.float32; the DiT keeps fp32)
+    noise      "numpy": generation_noise (bit-identical to the reference),
+               "device": on-device Philox N(0,1) (throughput mode)
+    """
+
+    def __init__(self, model: VelocityModel, sched: TimeWindowSchedule, n: int, num_streams: int = 1,
+                 cond: Conditioning | list | None = None, seed: int | list = 0, m: int | None = None,
+                 dtype=np.float64, noise: str = "numpy", use_graph: bool = True, device: str = "cuda"):
+        if not torch.cuda.is_available():
+            raise RuntimeError("StreamBatch needs a CUDA device; there is no CPU fallback")
+        _check_run_args(1 if m is None else m, n, sched)
+        if num_streams < 1:
+            raise ParameterError(f"need at least one stream, got {num_streams}")
+        if noise not in ("numpy", "device", "host"):
+            raise ParameterError(f"noise must be 'numpy', 'device' or 'host', got {noise!r}")
+        self.model, self.sched, self.n, self.S = model, sched, int(n), int(num_streams)
+        self.m = _UNBOUNDED if m is None else int(m)
+        self.noise, self.use_graph, self.device = noise, bool(use_graph), device
+        self.D = model.dim
+        self.kind = ("dit" if isinstance(model, DiTVelocityModel) else
+                     "mock" if isinstance(model, SeededMockModel) else "generic")
+        self.np_dtype = np.dtype(dtype)
+        if self.np_dtype not in (np.float32, np.float64):
+            raise ParameterError(f"unsupported latent dtype {dtype}")
+        if self.kind == "dit" and self.np_dtype != np.float32:
+            raise ParameterError("the DiT stream batch keeps fp32 latents; pass dtype=np.float32")
+        self.t_dtype = torch.float64 if self.np_dtype == np.float64 else torch.float32
+        conds = cond if isinstance(cond, (list, tuple)) else [cond] * self.S
+        if len(conds) != self.S or any(c is None for c in conds):
+            raise ParameterError("need one Conditioning (or a list of num_streams)")
+        ws = {c.guidance_scale for c in conds}
+        if len(ws) != 1:
+            raise ParameterError("all streams of one StreamBatch share the guidance scale")
+        self.w = float(ws.pop())
+        self.conds = conds
+        self.seeds = list(seed) if isinstance(seed, (list, tuple)) else [int(seed) + s for s in range(self.S)]
+        E = model.embed_dim
+        for c in conds:
+            if c.embed_dim != E:
+                raise ParameterError(f"embedding length {c.embed_dim} != model embed_dim {E}")
+        dev = device
+        R = self.S * self.n
+        if self.kind == "dit" and (2 if self.w != 1.0 else 1) * R > model.max_rows:
+            raise ParameterError(f"{R} slots (x2 with CFG) exceed the model's max_rows {model.max_rows}")
+        self.dsched = DeviceSchedule.of(sched)
+        self.stage_params = self.dsched.params(self.dsched.grid[: self.n].clone()).contiguous()
+        self.stage_times = np.asarray(sched.inference_grid[: self.n], dtype=np.float64).copy()
+        self.ctl = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.row_info = torch.zeros(R * 4, dtype=torch.int64, device=dev)
+        self.row_t = torch.zeros(R, dtype=torch.float64, device=dev)
+        self.x_ring = torch.zeros(R, self.D, dtype=self.t_dtype, device=dev)
+        self.frames = torch.zeros(self.S, self.D, dtype=self.t_dtype, device=dev)
+        self.frame_ids = torch.full((self.S,), -1, dtype=torch.int64, device=dev)
+        self.emb = torch.as_tensor(np.stack([c.embedding for c in conds]), dtype=torch.float64).to(dev).contiguous()
+        negs = [c.negative_embedding for c in conds]
+        self.neg = None if all(x is None for x in negs) else torch.as_tensor(
+            np.stack([np.zeros(E) if x is None else x for x in negs]), dtype=torch.float64).to(dev).contiguous()
+        noise_dt = torch.float32 if self.kind == "dit" else torch.float64
+        self.noise_dev = torch.zeros(self.S, self.D, dtype=noise_dt, device=dev)
+        self.noise_host = torch.zeros(self.S, self.D, dtype=noise_dt).pin_memory() if noise == "numpy" else None
+        self.noise_seed = int(self.seeds[0]) & ((1 << 64) - 1)
+        self._h2d_done = torch.cuda.Event()
+        self.stats = [RunStats() for _ in range(self.S)]
+        self.j = 0
+        self._stream = lambda: torch.cuda.current_stream().cuda_stream
+        self.reset()
+
+    # ------------------------------------------------------------------ admission noise
+    def _fill_noise(self, gen: int) -> bool:
+        """Stage generation `gen`'s initial noise for every stream; False if none."""
+        if gen >= self.m:
+            return False
+        if self.noise == "numpy":
+            arr = np.stack([generation_noise(sd, gen, self.D) for sd in self.seeds])
+            self._h2d_done.synchronize()  # the previous async copy has left the pinned buffer
+            self.noise_host.copy_(torch.from_numpy(arr.astype(self.noise_host.numpy().dtype, copy=False)))
+            self.noise_dev.copy_(self.noise_host, non_blocking=True)
+            self._h2d_done.record()
+        return True
+
+    def reset(self) -> None:
+        st = self._stream()
+        self.j = 0
+        self.stats = [RunStats() for _ in range(self.S)]
+        self._fill_noise(0)
+        use_host = self.noise == "numpy"
+        if self.kind == "dit":
+            _lib.call("sf_dit_stream_reset", self.ctl.data_ptr(), self.S, self.n, self.D, self.x_ring.data_ptr(),
+                      self.noise_dev.data_ptr() if use_host else None, self.noise_seed, st)
+        else:
+            if not use_host:
+                tmp = torch.empty(self.S, self.D, dtype=torch.float32, device=self.device)
+                _lib.call("sf_philox_normal", tmp.data_ptr(), self.S, self.D, self.noise_seed, 0, st)
+                self.noise_dev.copy_(tmp)
+            _lib.call("sf_stream_reset", self.ctl.data_ptr(), self.S, self.n, self.D,
+                      _lib.SF_F64 if self.t_dtype == torch.float64 else _lib.SF_F32, self.x_ring.data_ptr(),
+                      self.noise_dev.data_ptr(), st)
+
+    @property
+    def total_iterations(self) -> int:
+        return self.m + self.n - 1
+
+    def done(self) -> bool:
+        return self.j >= self.total_iterations
+
+    # ------------------------------------------------------------------ one iteration
+    def launch(self) -> int:
+        """Enqueue iteration j on the current CUDA stream without any host sync.
+        Returns the generation id retiring this iteration (or -1)."""
+        if self.done():
+            raise StateError("stream batch already drained all generations")
+        j, n, m, st = self.j, self.n, self.m, self._stream()
+        admit_next = self._fill_noise(j + 1) if self.noise == "numpy" else (j + 1 < m)
+        if self.kind == "dit":
+            _lib.call("sf_dit_stream_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, n, m,
+                      self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
+                      self.x_ring.data_ptr(), self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
+                      self.w, self.noise_dev.data_ptr() if self.noise != "device" else None, self.noise_seed,
+                      self.frames.data_ptr(), self.frame_ids.data_ptr(), 1 if self.use_graph else 0, st)
+        else:
+            if self.noise == "device" and admit_next:
+                tmp = torch.empty(self.S, self.D, dtype=torch.float32, device=self.device)
+                _lib.call("sf_philox_normal", tmp.data_ptr(), self.S, self.D, self.noise_seed, j + 1, st)
+                self.noise_dev.copy_(tmp)
+            _lib.call("sf_stream_prepare", self.ctl.data_ptr(), self.S, n, m, self.stage_params.data_ptr(),
+                      self.row_info.data_ptr(), self.row_t.data_ptr(), st)
+            if self.kind == "mock":
+                _lib.call("sf_stream_mock_step", self.ctl.data_ptr(), self.S, n, m, self.D,
+                          _lib.SF_F64 if self.t_dtype == torch.float64 else _lib.SF_F32, self.x_ring.data_ptr(),
+                          self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
+                          self.model.seed, self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
+                          self.model.embed_dim, self.w, self.noise_dev.data_ptr(), self.frames.data_ptr(),
+                          self.frame_ids.data_ptr(), st)
+            else:
+                self._generic_step(j)
+        lo, hi = max(0, j - n + 1), min(j, m - 1)
+        for s in range(self.S):
+            rs = self.stats[s]
+            rs.model_calls += 1
+            rs.scheduler_calls += 1
+            rs.step_stats.param_evals += hi - lo + 1
+            rs.step_stats.elementwise_ops += 3
+            rs.step_stats.scheduler_calls += 1
+        self.j += 1
+        retiring = j - n + 1
+        if 0 <= retiring < m:
+            for rs in self.stats:
+                rs.decodes += 1
+            return retiring
+        return -1
+
+    def _generic_step(self, j: int) -> None:
+        """Any VelocityModel: gather the active rows (newest first), one guided
+        forward, device Euler, scatter back, emit, refill."""
+        n, m = self.n, self.m
+        lo, hi = max(0, j - n + 1), min(j, m - 1)
+        gens = list(range(hi, lo - 1, -1))
+        rows = [s * n + g % n for s in range(self.S) for g in gens]
+        idx = torch.tensor(rows, device=self.device)
+        stages = torch.tensor([j - g for _ in range(self.S) for g in gens], device=self.device)
+        x = self.x_ring.index_select(0, idx)
+        ts = self.dsched.grid.index_select(0, stages)
+        ids = torch.tensor([g for _ in range(self.S) for g in gens], device=self.device)
+        eps_rows = []
+        per = len(gens)
+        for s, c in enumerate(self.conds):
+            b = LatentBatch(data=x[s * per:(s + 1) * per], timesteps=ts[s * per:(s + 1) * per],
+                            ids=ids[s * per:(s + 1) * per])
+            if c.guidance_scale != 1.0:
+                d2, c2 = apply_cfg(b, c)
+                out = handle_cfg(self.model.forward(d2, c2), c.guidance_scale)
+            else:
+                out = self.model.forward(b, c)
+            e = out.epsilon if isinstance(out.epsilon, torch.Tensor) else torch.from_numpy(out.epsilon).cuda()
+            eps_rows.append(e.to(self.x_ring.dtype) if e.dtype not in (torch.float32, torch.float64) else e)
+        eps = torch.cat(eps_rows)
+        params = self.stage_params.index_select(0, stages).contiguous()
+        x_new = velocity_step_device(eps.contiguous(), x.contiguous(), params)
+        self.x_ring.index_copy_(0, idx, x_new)
+        retiring = j - n + 1
+        if 0 <= retiring < m:
+            for s in range(self.S):
+                self.frames[s].copy_(self.x_ring[s * n + retiring % n])
+            self.frame_ids.fill_(retiring)
+        else:
+            self.frame_ids.fill_(-1)
+        if j + 1 < m:
+            k = (j + 1) % n
+            for s in range(self.S):
+                self.x_ring[s * n + k].copy_(self.noise_dev[s].to(self.x_ring.dtype))
+
+    def launch_host_io(self, noise_src: torch.Tensor, frames_dst: torch.Tensor) -> int:
+        """End-to-end serving step with HOST buffers (noise="host"): async H2D of
+        the admitted generation's noise from pinned ``noise_src`` [S, D], the
+        device step, async D2H of the emitted frames into pinned ``frames_dst``.
+        All three are ordered on the current stream; no host sync."""
+        self.noise_dev.copy_(noise_src, non_blocking=True)
+        g = self.launch()
+        frames_dst.copy_(self.frames, non_blocking=True)
+        return g
+
+    def profile_step(self) -> dict:
+        """One eager DiT step with a CUDA event after every launch: per kernel
+        class {name: (total_ms, launches)} (sf_dit_profile_step)."""
+        if self.kind != "dit":
+            raise StateError("profile_step is implemented for the DiT stream batch")
+        from .dit import PROFILE_CLASSES
+
+        ms = (C.c_float * 16)()
+        cnt = (C.c_int32 * 16)()
+        j = self.j
+        _lib.call("sf_dit_profile_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, self.n, self.m,
+                  self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
+                  self.x_ring.data_ptr(), self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
+                  self.w, self.noise_dev.data_ptr() if self.noise != "device" else None, self.noise_seed,
+                  self.frames.data_ptr(), self.frame_ids.data_ptr(), ms, cnt, self._stream())
+        self.j = j + 1
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PROFILE_CLASSES)}
+
+    def step(self, decode_cost_us: float = 0.0) -> list:
+        """One iteration; returns [(stream, GenerationResult)] for the frames that
+        retired (one per stream after warm-up), copied to the host."""
+        g = self.launch()
+        if g < 0:
+            return []
+        frames = self.frames.cpu().numpy()
+        out = []
+        for s in range(self.S):
+            lat = frames[s].copy()
+            self.stats[s].decode_time_us += decode_cost_us
+            out.append((s, GenerationResult(id=g, latent=lat, decoded=decode_stub(lat, decode_cost_us),
+                                            iterations_spanned=self.n)))
+        return out
+
+    def __call__(self, m: int | None = None) -> list:
+        """Run to completion (m generations per stream); results per stream in
+        completion order."""
+        if m is not None and m != self.m:
+            _check_run_args(m, self.n, self.sched)
+            self.m = int(m)
+            self.reset()
+        if self.m == _UNBOUNDED:
+            raise ParameterError("an unbounded StreamBatch has no completion; call step()")
+        res = [[] for _ in range(self.S)]
+        while not self.done():
+            for s, r in self.step():
+                res[s].append(r)
+        return res
+
+    def snapshot(self, emitted: int) -> PipelineState:
+        """Newest-first buffer of stream 0 after the last iteration (pipeline.py:208-219)."""
+        j = self.j - 1
+        n, m = self.n, self.m
+        lo, hi = max(0, j - n + 1), min(j, m - 1)
+        ring = self.x_ring[:n].cpu().numpy()
+        buf = []
+        for g in range(hi, lo - 1, -1):
+            stage = j - g + 1
+            if stage >= n:
+                continue
+            buf.append(BufferEntry(latent=ring[g % n].copy(), gen_id=g, stage=stage))
+        return PipelineState(buffer=buf, stage_times=self.stage_times, emitted=emitted, iteration=j)
+
+
+# ----------------------------------------------------------------------------- reference entry points
+def run_stream(m: int, n: int, model: VelocityModel, cond: Conditioning, seed: int, sched: TimeWindowSchedule,
+               sched_cost_us: float = 0.0, decode_cost_us: float = 0.0, dtype=np.float64,
+               on_iteration: Callable[[PipelineState], None] | None = None):
+    """pipeline.py:139-220: m generations of n steps in m+n-1 iterations,
+    through the device-resident stream batch (one stream)."""
+    _check_run_args(m, n, sched)
+    if isinstance(model, DiTVelocityModel) and np.dtype(dtype) == np.float64:
+        dtype = np.float32  # the DiT ring is fp32 (documented in DESIGN.md)
+    sb = StreamBatch(model, sched, n, num_streams=1, cond=cond, seed=seed, m=m, dtype=dtype, noise="numpy")
+    results = []
+    while not sb.done():
+        busy_wait_us(sched_cost_us)
+        for _, r in sb.step(decode_cost_us):
+            results.append(r)
+        if on_iteration is not None:
+            on_iteration(sb.snapshot(len(results)))
+    return results, sb.stats[0]
+
+
+def run_vanilla(m: int, n: int, model: VelocityModel, cond: Conditioning, seed: int, sched: TimeWindowSchedule,
+                sched_cost_us: float = 0.0, decode_cost_us: float = 0.0):
+    """pipeline.py:223-266: one generation at a time, m*n single-row calls."""
+    _check_run_args(m, n, sched)
+    stats = RunStats()
+    results = []
+    for g in range(m):
+        latent = generation_noise(seed, g, model.dim)
+        t = float(sched.inference_grid[0])
+        for _ in range(n):
+            batch = LatentBatch(data=latent[None, :], timesteps=np.asarray([t]), ids=np.asarray([g], dtype=np.int64))
+            if cond.guidance_scale != 1.0:
+                d2, c2 = apply_cfg(batch, cond)
+                eps = handle_cfg(model.forward(d2, c2), cond.guidance_scale).epsilon
+            else:
+                eps = model.forward(batch, cond).epsilon
+            stats.model_calls += 1
+            busy_wait_us(sched_cost_us)
+            latent, t = sequential_velocity_step(np.asarray(eps)[0], latent, t, sched, stats.step_stats)
+            stats.scheduler_calls += 1
+        stats.decodes += 1
+        stats.decode_time_us += decode_cost_us
+        results.append(GenerationResult(id=g, latent=latent, decoded=decode_stub(latent, decode_cost_us),
+                                        iterations_spanned=n))
+    return results, stats
