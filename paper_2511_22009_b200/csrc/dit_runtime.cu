@@ -10,6 +10,7 @@
 // The handle owns host-side state only (config, TMA descriptors, graph
 // cache).  All device memory (weights, workspace, ring state) is owned by the
 // caller and passed as raw pointers.
+#include <algorithm>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -111,104 +112,119 @@ __global__ void cond_kernel(RowSrc src, int hidden, int freq_dim, const __nv_bfl
 }
 
 // ============================================================ K2+K4: patch embed + pos + LN1 modulate
-// One warp per token; lane owns columns 128u + 4 lane + {0..3}, u < hidden/128.
+// One warp per token (grid-stride over tokens); lane owns columns
+// 128u + 4 lane + {0..3}.  Weights live in smem transposed ([PK][HID]) so a
+// warp's float4 reads are consecutive (conflict-free).
 template <int HID>
-__global__ void patch_embed_ln_kernel(const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C,
-                                      const __nv_bfloat16* __restrict__ pw, const float* __restrict__ pb,
-                                      const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
-                                      float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod,
-                                      int64_t total_tokens) {
+__global__ void __launch_bounds__(256) patch_embed_ln_kernel(
+    const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
+    const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
+    float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
   constexpr int U = HID / 128;
-  extern __shared__ float sw[];  // [HID][PK] fp32
-  const int PK = C * P * P;
-  for (int idx = threadIdx.x; idx < HID * PK; idx += blockDim.x) sw[idx] = __bfloat162float(pw[idx]);
+  constexpr int PK = 16;  // C * P * P (4 * 2 * 2), checked at create
+  extern __shared__ float swT[];  // [PK][HID]
+  for (int idx = threadIdx.x; idx < HID * PK; idx += blockDim.x) {
+    const int nn = idx / PK, k = idx % PK;  // pw is [HID][PK]
+    swT[k * HID + nn] = __bfloat162float(pw[idx]);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (tok >= total_tokens) return;
   const int gw = HW / P, T = gw * gw;
-  const int64_t ni = tok / T;
-  const int tau = (int)(tok % T);
-  const int pi = tau / gw, pj = tau % gw;
-  const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
-  float v[16];
-  for (int c = 0; c < C; ++c)
-    for (int p = 0; p < P; ++p)
-      for (int q = 0; q < P; ++q) v[(c * P + p) * P + q] = xl[(int64_t)c * HW * HW + (pi * P + p) * HW + pj * P + q];
-  float y[U][4];
-  float sum = 0.f;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < total_tokens; tok += wstride) {
+    const int64_t ni = tok / T;
+    const int tau = (int)(tok % T);
+    const int pi = tau / gw, pj = tau % gw;
+    const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
+    float v[PK];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n0 = 128 * u + 4 * lane;
-    const float4 bb = *reinterpret_cast<const float4*>(pb + n0);
-    const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)tau * HID + n0);
-    float a[4] = {bb.x + pp.x, bb.y + pp.y, bb.z + pp.z, bb.w + pp.w};
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      float acc = 0.f;
-      for (int k = 0; k < PK; ++k) acc += v[k] * sw[(n0 + r) * PK + k];
-      const float val = __bfloat162float(__float2bfloat16_rn(acc + a[r]));  // residual stored bf16
-      y[u][r] = val;
-      sum += val;
+      for (int p = 0; p < 2; ++p) {
+        const float2 t2 = *reinterpret_cast<const float2*>(xl + (int64_t)c * HW * HW + (pi * 2 + p) * HW + pj * 2);
+        v[(c * 2 + p) * 2 + 0] = t2.x;
+        v[(c * 2 + p) * 2 + 1] = t2.y;
+      }
+    float y[U][4];
+    float sum = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n0 = 128 * u + 4 * lane;
+      const float4 bb = *reinterpret_cast<const float4*>(pb + n0);
+      const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)tau * HID + n0);
+      float a0 = bb.x + pp.x, a1 = bb.y + pp.y, a2 = bb.z + pp.z, a3 = bb.w + pp.w;
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < PK; ++k) {
+        const float4 wv = *reinterpret_cast<const float4*>(swT + k * HID + n0);
+        c0 += v[k] * wv.x;
+        c1 += v[k] * wv.y;
+        c2 += v[k] * wv.z;
+        c3 += v[k] * wv.w;
+      }
+      y[u][0] = __bfloat162float(__float2bfloat16_rn(c0 + a0));  // residual stored bf16
+      y[u][1] = __bfloat162float(__float2bfloat16_rn(c1 + a1));
+      y[u][2] = __bfloat162float(__float2bfloat16_rn(c2 + a2));
+      y[u][3] = __bfloat162float(__float2bfloat16_rn(c3 + a3));
+      sum += (y[u][0] + y[u][1]) + (y[u][2] + y[u][3]);
     }
-  }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float mean = sum / HID;
-  float var = 0.f;
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / HID;
+    float var = 0.f;
 #pragma unroll
-  for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
+      for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-  const float rstd = rsqrtf(var / HID + ln_eps);
-  const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
-  const float* scale = shift + HID;
+    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float rstd = rsqrtf(var / HID + ln_eps);
+    const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
+    const float* scale = shift + HID;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int n0 = 128 * u + 4 * lane;
-    const float4 sh = *reinterpret_cast<const float4*>(shift + n0);
-    const float4 sc = *reinterpret_cast<const float4*>(scale + n0);
-    const float shv[4] = {sh.x, sh.y, sh.z, sh.w}, scv[4] = {sc.x, sc.y, sc.z, sc.w};
-    float o[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) o[r] = (y[u][r] - mean) * rstd * (1.0f + scv[r]) + shv[r];
-    *reinterpret_cast<uint2*>(xres + tok * HID + n0) = make_uint2(pack_bf16(y[u][0], y[u][1]), pack_bf16(y[u][2], y[u][3]));
-    *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]));
+    for (int u = 0; u < U; ++u) {
+      const int n0 = 128 * u + 4 * lane;
+      const float4 sh = *reinterpret_cast<const float4*>(shift + n0);
+      const float4 sc = *reinterpret_cast<const float4*>(scale + n0);
+      const float o0 = (y[u][0] - mean) * rstd * (1.0f + sc.x) + sh.x;
+      const float o1 = (y[u][1] - mean) * rstd * (1.0f + sc.y) + sh.y;
+      const float o2 = (y[u][2] - mean) * rstd * (1.0f + sc.z) + sh.z;
+      const float o3 = (y[u][3] - mean) * rstd * (1.0f + sc.w) + sh.w;
+      *reinterpret_cast<uint2*>(xres + tok * HID + n0) =
+          make_uint2(pack_bf16(y[u][0], y[u][1]), pack_bf16(y[u][2], y[u][3]));
+      *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+    }
   }
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
-struct StepCoefF {
-  float lam, eta, span, dt;
-  bool at_end;
-};
-
+// One warp per token (grid-stride).  16 output features per token: lane f < 16
+// ends up owning feature f = (p*2 + q)*4 + c, i.e. one latent pixel.
 template <int HID, bool STREAM>
-__global__ void final_layer_kernel(const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw,
-                                   const float* __restrict__ fb, int HW, int P, int C, int64_t lat_rows,
-                                   // direct mode
-                                   float* __restrict__ eps_out,
-                                   // stream mode
-                                   const int64_t* __restrict__ ctl, int n, int64_t m, const double* __restrict__ stage_params,
-                                   const int64_t* __restrict__ row_info, int cfg, float w, float* __restrict__ x_ring,
-                                   const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
-                                   int64_t* __restrict__ frame_ids, int64_t total_tokens) {
+__global__ void __launch_bounds__(256) final_layer_kernel(
+    const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
+    int P, int C, int64_t lat_rows,
+    // direct mode
+    float* __restrict__ eps_out,
+    // stream mode
+    const int64_t* __restrict__ ctl, int n, int64_t m, const double* __restrict__ stage_params,
+    const int64_t* __restrict__ row_info, int cfg, float w, float* __restrict__ x_ring,
+    const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
+    int64_t* __restrict__ frame_ids, int64_t total_tokens) {
   constexpr int U = HID / 128;
-  const int PK = C * P * P;  // 16 outputs per token
+  constexpr int PK = 16;
   extern __shared__ float sw[];  // [PK][HID] + bias[PK]
   for (int idx = threadIdx.x; idx < PK * HID; idx += blockDim.x) sw[idx] = __bfloat162float(fw[idx]);
   for (int idx = threadIdx.x; idx < PK; idx += blockDim.x) sw[PK * HID + idx] = fb[idx];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // over lat_rows * T
-  if (tok >= total_tokens) return;
   const int gw = HW / P, T = gw * gw;
-  const int64_t lr = tok / T;
-  const int tau = (int)(tok % T);
+  const int64_t D = (int64_t)C * HW * HW;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
+  int64_t j = 0;
+  if constexpr (STREAM) j = ctl[1];
 
-  auto project = [&](int64_t net_row, float (&eo)[16]) {
+  auto project = [&](int64_t net_row, int tau) -> float {
     const __nv_bfloat16* xr = xmod + (net_row * T + tau) * HID;
     float xv[U][4];
 #pragma unroll
@@ -220,76 +236,67 @@ __global__ void final_layer_kernel(const __nv_bfloat16* __restrict__ xmod, const
       xv[u][2] = b.x;
       xv[u][3] = b.y;
     }
+    float mine = 0.f;
 #pragma unroll
-    for (int f = 0; f < 16; ++f) {
+    for (int f = 0; f < PK; ++f) {
       float acc = 0.f;
-      if (f < PK) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) acc += xv[u][r] * sw[f * HID + 128 * u + 4 * lane + r];
+      for (int u = 0; u < U; ++u) {
+        const float4 wv = *reinterpret_cast<const float4*>(sw + f * HID + 128 * u + 4 * lane);
+        acc += xv[u][0] * wv.x + xv[u][1] * wv.y + xv[u][2] * wv.z + xv[u][3] * wv.w;
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      eo[f] = acc;
+      if (lane == f) mine = acc;
     }
+    return mine + (lane < PK ? sw[PK * HID + lane] : 0.f);
   };
 
-  float ec[16];
-  project(STREAM && cfg ? lr + lat_rows : lr, ec);
-  float e = 0.f;
-#pragma unroll
-  for (int f = 0; f < 16; ++f)
-    if (lane == f) e = ec[f];
-  if (lane < PK) e += sw[PK * HID + lane];
-  if constexpr (STREAM) {
-    if (cfg) {
-      float eu_all[16];
-      project(lr, eu_all);
-      float eu = 0.f;
-#pragma unroll
-      for (int f = 0; f < 16; ++f)
-        if (lane == f) eu = eu_all[f];
-      if (lane < PK) eu += sw[PK * HID + lane];
-      e = __fadd_rn(eu, __fmul_rn(w, __fsub_rn(e, eu)));  // handle_cfg (models.py:288-293)
+  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < total_tokens; tok += wstride) {
+    const int64_t lr = tok / T;
+    const int tau = (int)(tok % T);
+    float e = project(STREAM && cfg ? lr + lat_rows : lr, tau);
+    if constexpr (STREAM) {
+      if (cfg) {
+        const float eu = project(lr, tau);
+        e = __fadd_rn(eu, __fmul_rn(w, __fsub_rn(e, eu)));  // handle_cfg (models.py:288-293)
+      }
     }
-  }
-  if (lane >= PK) return;
-  // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
-  const int c = lane % C, q = (lane / C) % P, p = lane / (C * P);
-  const int pi = tau / gw, pj = tau % gw;
-  const int64_t D = (int64_t)C * HW * HW;
-  const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
-  if constexpr (!STREAM) {
-    eps_out[lr * D + idx] = e;
-  } else {
-    const int64_t j = ctl[1];
-    const int64_t stage = row_info[lr * 4 + 0];
-    const int64_t g = row_info[lr * 4 + 1];
-    const bool active = row_info[lr * 4 + 2] != 0;
-    const int64_t s = row_info[lr * 4 + 3];
-    const int64_t k = lr % n;
-    const bool refill_slot = (k == (j + 1) % n);
-    const bool admit = refill_slot && (j + 1 < m);
-    const bool retiring = active && (stage + 1 == n);
-    if (refill_slot && tau == 0 && lane == 0) frame_ids[s] = retiring ? g : -1;
-    float* xr = x_ring + lr * D;
-    const float noise = admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx))
-                              : 0.0f;
-    if (active) {
-      const double* p = stage_params + stage * SF_PARAM_STRIDE;
-      const float lam = __double2float_rn(p[SF_P_LAMBDA_T]), eta = __double2float_rn(p[SF_P_ETA_T]);
-      const float span = __double2float_rn(p[SF_P_SPAN]), dt = __double2float_rn(p[SF_P_DT]);
-      const bool at_end = p[SF_P_AT_END] != 0.0;
-      const float x = xr[idx];
-      // velocity.py:125-130 in fp32
-      const float x_pred = __fadd_rn(__fmul_rn(lam, x), __fmul_rn(eta, e));
-      const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, x), span);
-      const float xn = __fadd_rn(x, __fmul_rn(dt, v));
-      if (retiring) frames_out[s * D + idx] = xn;
-      xr[idx] = admit ? noise : xn;
-    } else if (admit) {
-      xr[idx] = noise;
+    if (lane >= PK) continue;
+    // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
+    const int c = lane % C, q = (lane / C) % P, p = lane / (C * P);
+    const int pi = tau / gw, pj = tau % gw;
+    const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
+    if constexpr (!STREAM) {
+      eps_out[lr * D + idx] = e;
+    } else {
+      const int64_t stage = row_info[lr * 4 + 0];
+      const int64_t g = row_info[lr * 4 + 1];
+      const bool active = row_info[lr * 4 + 2] != 0;
+      const int64_t s = row_info[lr * 4 + 3];
+      const int64_t k = lr % n;
+      const bool refill_slot = (k == (j + 1) % n);
+      const bool admit = refill_slot && (j + 1 < m);
+      const bool retiring = active && (stage + 1 == n);
+      if (refill_slot && tau == 0 && lane == 0) frame_ids[s] = retiring ? g : -1;
+      float* xr = x_ring + lr * D;
+      const float noise =
+          admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
+      if (active) {
+        const double* pp = stage_params + stage * SF_PARAM_STRIDE;
+        const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
+        const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
+        const bool at_end = pp[SF_P_AT_END] != 0.0;
+        const float xo = xr[idx];
+        // velocity.py:125-130 in fp32
+        const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
+        const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
+        const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
+        if (retiring) frames_out[s * D + idx] = xn;
+        xr[idx] = admit ? noise : xn;
+      } else if (admit) {
+        xr[idx] = noise;
+      }
     }
   }
 }
@@ -480,7 +487,7 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   const sf_dit_config& c = h->cfg;
   const int64_t tokens = rows * h->tokens;
   const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
-  const unsigned blocks = (unsigned)((tokens + 7) / 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8);
   patch_embed_ln_kernel<384><<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch,
                                                       (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b,
                                                       h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres,
@@ -590,7 +597,7 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if ((rc = launch_patch(h, x, rows, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = rows * h->tokens;
-  final_layer_kernel<384, false><<<(unsigned)((tokens + 7) / 8), 256, final_smem(c), st>>>(
+  final_layer_kernel<384, false><<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, rows, eps_out,
       nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr, tokens);
   return cuda_status();
@@ -613,7 +620,7 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = R * h->tokens;
-  final_layer_kernel<384, true><<<(unsigned)((tokens + 7) / 8), 256, final_smem(c), st>>>(
+  final_layer_kernel<384, true><<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
       m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
   mark(h, P_FINAL, st);
