@@ -193,7 +193,10 @@ def main():
     rows = S * n * (2 if w != 1.0 else 1)
     model = sf.DiTVelocityModel(cfg, seed=0, max_rows=rows)
     sched = sf.build_time_window_schedule(num_windows=args.windows, inference_steps=n)
-    seeds = [1000 + rank * S + s for s in range(S)]
+    from paper_2511_22009_b200.partition import gather_frames, reduce_counts, stream_partition, stream_seeds
+
+    mine = stream_partition(S * world, world, rank)  # weak scaling: S streams per GPU
+    seeds = stream_seeds(1000, mine)
     conds = [sf.make_conditioning(np.random.default_rng([sd, 2**32 - 1]).standard_normal(cfg.embed_dim),
                                   guidance_scale=w) for sd in seeds]
     sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, dtype=np.float32, noise="device")
@@ -276,11 +279,10 @@ def main():
     # ---- stream-partitioned output: NCCL gather of the last frames + frame counts (off the timed region)
     gathered = None
     if world > 1:
-        out = torch.empty(world * S, cfg.dim, device="cuda")
-        dist.all_gather_into_tensor(out, sb.frames.contiguous())
-        cnt = torch.tensor([float(frames / world)], device="cuda")
-        dist.all_reduce(cnt)
-        gathered = {"frames_gathered_rank0": int(out.shape[0]), "frames_total": int(cnt.item())}
+        allf, ids = gather_frames(sb.frames, sb.frame_ids)
+        cnt = reduce_counts([S * args.steps, sb.stats[0].model_calls], "cuda")
+        gathered = {"frames_gathered": int(allf.shape[0]), "frame_ids_valid": int((ids >= 0).sum().item()),
+                    "frames_emitted_timed_total": cnt[0]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

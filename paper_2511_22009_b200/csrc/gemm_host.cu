@@ -38,11 +38,17 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 }
 
 template <int BN, int KIND>
+constexpr int epi_warps() {
+  return KIND == EPI_RES_LN || KIND == EPI_QKV ? 4 : 8;
+}
+
+template <int BN, int KIND>
 static int set_attr() {
   static bool done = false;
   if (!done) {
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<BN>::SMEM_BYTES) != cudaSuccess)
+    constexpr int W = epi_warps<BN, KIND>();
+    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GemmCfg<BN, W>::SMEM_BYTES) != cudaSuccess)
       return SF_ERR_CUDA;
     done = true;
   }
@@ -63,13 +69,28 @@ int prepare_gemm_kernels() {
   return rc;
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int BN, int KIND>
 static int launch_one(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, const EpiParams& ep,
                       cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  constexpr int W = epi_warps<BN, KIND>();
+  using C = GemmCfg<BN, W>;
   if (set_attr<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
-  dim3 grid(N / BN, (M + C::BM - 1) / C::BM);
-  gemm_bf16_tcgen05<BN, KIND><<<grid, 192, C::SMEM_BYTES, st>>>(a, b, K, ep);
+  const int tiles = (N / BN) * ((M + C::BM - 1) / C::BM);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  EpiParams e = ep;
+  e.M = M;
+  gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, N, K, e);
   return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
 
