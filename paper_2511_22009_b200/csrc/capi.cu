@@ -1,4 +1,4 @@
-// Misc C-ABI entry points: version, device query, standalone GEMM.
+// Misc C-ABI entry points: version, device query, standalone GEMMs.
 #include "gemm_tcgen05.cuh"
 #include "sf_internal.h"
 
@@ -18,50 +18,50 @@ int sf_device_sm_count(void) {
 int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
                  int32_t epi, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % 128) return SF_ERR_PARAMETER;
+  const int no_store = (epi & 0x100) ? 1 : 0;  // diagnostics flag (not part of the documented ABI values)
+  epi &= 0xff;
   if (epi < EPI_F32 || epi > EPI_GELU) return SF_ERR_PARAMETER;
   const int bn = (N % 256 == 0) ? 256 : 128;
-  CUtensorMap ta, tb;
-  if (make_tmap_bf16_2d(&ta, A, K, M, K, 64, 128) != SF_OK) return SF_ERR_CUDA;
-  if (make_tmap_bf16_2d(&tb, W, K, N, K, 64, gemm_b_box_rows(bn)) != SF_OK) return SF_ERR_CUDA;
+  GemmMaps maps;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if (epi != EPI_F32 && make_out_map(&maps.d[0], C, M, N) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
   ep.out = C;
   ep.ldo = N;
   ep.tokens_per_slot = 1 << 30;
   ep.M = (int)M;
-  return launch_gemm(epi, bn, ta, tb, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  ep.no_store = no_store;
+  return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
 int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,
                 int32_t T, float q_scale, void* stream) {
   const int64_t d = (int64_t)heads * 64, N = 3 * d, K = d;
   if (M < 1 || M % T || T % 128 || N % 192 || K % 64) return SF_ERR_PARAMETER;
-  CUtensorMap ta, tb;
-  if (make_tmap_bf16_2d(&ta, A, K, M, K, 64, 128) != SF_OK) return SF_ERR_CUDA;
-  if (make_tmap_bf16_2d(&tb, W, K, N, K, 64, gemm_b_box_rows(192)) != SF_OK) return SF_ERR_CUDA;
+  GemmMaps maps;
+  if (make_operand_maps(&maps, A, M, K, W, N, 192) != SF_OK) return SF_ERR_CUDA;
+  if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
-  ep.q = (__nv_bfloat16*)q;
-  ep.k = (__nv_bfloat16*)k;
-  ep.vt = (__nv_bfloat16*)vt;
   ep.heads = heads;
   ep.q_scale = q_scale;
   ep.tokens_per_slot = T;
   ep.M = (int)M;
-  return launch_gemm(EPI_QKV, 192, ta, tb, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(EPI_QKV, 192, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
 int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, void* xmod, const float* gate,
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream) {
   if (N != 384 || K % 64 || M < 1 || M % tokens_per_slot || tokens_per_slot % 128) return SF_ERR_PARAMETER;
-  CUtensorMap ta, tb;
-  if (make_tmap_bf16_2d(&ta, A, K, M, K, 64, 128) != SF_OK) return SF_ERR_CUDA;
-  if (make_tmap_bf16_2d(&tb, W, K, N, K, 64, gemm_b_box_rows(384)) != SF_OK) return SF_ERR_CUDA;
+  GemmMaps maps;
+  if (make_operand_maps(&maps, A, M, K, W, N, 384) != SF_OK) return SF_ERR_CUDA;
+  if (make_out_map(&maps.d[0], xres, M, N) != SF_OK || make_out_map(&maps.d[1], xmod, M, N) != SF_OK)
+    return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
-  ep.xres = (__nv_bfloat16*)xres;
-  ep.xmod = (__nv_bfloat16*)xmod;
+  ep.xres = (const __nv_bfloat16*)xres;
   ep.gate = gate;
   ep.shift = shift;
   ep.scale = scale;
@@ -69,7 +69,7 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
   ep.ln_eps = ln_eps;
   ep.tokens_per_slot = tokens_per_slot;
   ep.M = (int)M;
-  return launch_gemm(EPI_RES_LN, 384, ta, tb, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(EPI_RES_LN, 384, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -333,8 +333,8 @@ struct sf_dit {
   __nv_bfloat16 *cond, *xres, *xmod, *q, *k, *vt, *attn, *hmid;
   float* mod;
   // TMA descriptors
-  CUtensorMap a_cond, a_xmod, a_attn, a_hmid, b_ada;
-  std::vector<CUtensorMap> b_qkv, b_proj, b_fc1, b_fc2;
+  GemmMaps g_ada;                                  // TMA descriptors per GEMM call site
+  std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
   AttnMaps attn_maps;
   std::map<std::tuple<const void*, int64_t, int, int64_t, double, const void*, const void*, const void*>,
            cudaGraphExec_t>
@@ -399,7 +399,7 @@ static int run_forward_core(sf_dit* h, int64_t rows, cudaStream_t st) {
     ep.ldo = h->mod_stride;
     ep.tokens_per_slot = 1 << 30;
     ep.M = (int)rows;
-    if ((rc = launch_gemm(EPI_F32, 256, h->a_cond, h->b_ada, (int)rows, (int)h->mod_stride, H, ep, st))) return rc;
+    if ((rc = launch_gemm(EPI_F32, 256, h->g_ada, (int)rows, (int)h->mod_stride, H, ep, st))) return rc;
     mark(h, P_ADALN, st);
   }
   return SF_OK;
@@ -415,14 +415,11 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
     {
       EpiParams ep{};
       ep.bias = h->w.qkv_b + (int64_t)l * 3 * H;
-      ep.q = h->q;
-      ep.k = h->k;
-      ep.vt = h->vt;
       ep.heads = c.heads;
       ep.q_scale = 0.125f;  // 1/sqrt(64)
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_QKV, 192, h->a_xmod, h->b_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_QKV, 192, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
       mark(h, P_QKV, st);
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
@@ -431,7 +428,6 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       EpiParams ep{};
       ep.bias = h->w.proj_b + (int64_t)l * H;
       ep.xres = h->xres;
-      ep.xmod = h->xmod;
       ep.gate = h->mod + l * B6 + 2 * H;   // gate_msa
       ep.shift = h->mod + l * B6 + 3 * H;  // shift_mlp
       ep.scale = h->mod + l * B6 + 4 * H;  // scale_mlp
@@ -439,24 +435,22 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.ln_eps = c.ln_eps;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_attn, h->b_proj[l], (int)M, H, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_RES_LN, 384, h->g_proj[l], (int)M, H, H, ep, st))) return rc;
       mark(h, P_PROJ, st);
     }
     {
       EpiParams ep{};
       ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
-      ep.out = h->hmid;
       ep.ldo = c.mlp_hidden;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_GELU, 256, h->a_xmod, h->b_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_GELU, 256, h->g_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
       mark(h, P_FC1, st);
     }
     {
       EpiParams ep{};
       ep.bias = h->w.fc2_b + (int64_t)l * H;
       ep.xres = h->xres;
-      ep.xmod = h->xmod;
       ep.gate = h->mod + l * B6 + 5 * H;  // gate_mlp
       const float* nxt = (l + 1 < c.depth) ? h->mod + (l + 1) * B6  // next block: shift_msa, scale_msa
                                            : h->mod + c.depth * B6;  // final layer: shift, scale
@@ -466,7 +460,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.ln_eps = c.ln_eps;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_RES_LN, 384, h->a_hmid, h->b_fc2[l], (int)M, H, c.mlp_hidden, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_RES_LN, 384, h->g_fc2[l], (int)M, H, c.mlp_hidden, ep, st))) return rc;
       mark(h, P_FC2, st);
     }
   }
@@ -538,24 +532,26 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
   const int64_t M = max_rows * h->tokens;
   const int64_t rows_pad = align_up(max_rows, 128);
   int rc = SF_OK;
-  rc |= make_tmap_bf16_2d(&h->a_cond, h->cond, H, rows_pad, H, 64, 128);
-  rc |= make_tmap_bf16_2d(&h->a_xmod, h->xmod, H, M, H, 64, 128);
-  rc |= make_tmap_bf16_2d(&h->a_attn, h->attn, H, M, H, 64, 128);
-  rc |= make_tmap_bf16_2d(&h->a_hmid, h->hmid, c.mlp_hidden, M, c.mlp_hidden, 64, 128);
-  rc |= make_tmap_bf16_2d(&h->b_ada, w->ada_w, H, h->mod_stride, H, 64, gemm_b_box_rows(256));
-  h->b_qkv.resize(c.depth);
-  h->b_proj.resize(c.depth);
-  h->b_fc1.resize(c.depth);
-  h->b_fc2.resize(c.depth);
+  rc |= make_operand_maps(&h->g_ada, h->cond, rows_pad, H, w->ada_w, h->mod_stride, 256);
+  h->g_qkv.resize(c.depth);
+  h->g_proj.resize(c.depth);
+  h->g_fc1.resize(c.depth);
+  h->g_fc2.resize(c.depth);
   for (int l = 0; l < c.depth; ++l) {
     const __nv_bfloat16* qkv = (const __nv_bfloat16*)w->qkv_w + (int64_t)l * 3 * H * H;
     const __nv_bfloat16* proj = (const __nv_bfloat16*)w->proj_w + (int64_t)l * H * H;
     const __nv_bfloat16* fc1 = (const __nv_bfloat16*)w->fc1_w + (int64_t)l * c.mlp_hidden * H;
     const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
-    rc |= make_tmap_bf16_2d(&h->b_qkv[l], qkv, H, 3 * H, H, 64, gemm_b_box_rows(192));
-    rc |= make_tmap_bf16_2d(&h->b_proj[l], proj, H, H, H, 64, gemm_b_box_rows(384));
-    rc |= make_tmap_bf16_2d(&h->b_fc1[l], fc1, H, c.mlp_hidden, H, 64, gemm_b_box_rows(256));
-    rc |= make_tmap_bf16_2d(&h->b_fc2[l], fc2, c.mlp_hidden, H, c.mlp_hidden, 64, gemm_b_box_rows(384));
+    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, 192);
+    rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
+    rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
+    rc |= make_out_map(&h->g_proj[l].d[0], h->xres, M, H);
+    rc |= make_out_map(&h->g_proj[l].d[1], h->xmod, M, H);
+    rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
+    rc |= make_out_map(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);
+    rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 384);
+    rc |= make_out_map(&h->g_fc2[l].d[0], h->xres, M, H);
+    rc |= make_out_map(&h->g_fc2[l].d[1], h->xmod, M, H);
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
   if (rc != SF_OK) {

@@ -22,24 +22,53 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Row-major bf16 matrix [outer, inner] -> 2-D tiled map with a (box_inner x
-// box_outer) box and 128-byte swizzle (box_inner * 2 must be 128).
+// box_outer) box; box_inner * 2 bytes must equal the swizzle width (32/64/128).
 int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
-                      uint32_t box_inner, uint32_t box_outer) {
+                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
   auto fn = encode_fn();
   if (!fn) return SF_ERR_CUDA;
+  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_stride_elems * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? SF_OK : SF_ERR_CUDA;
 }
 
+int gemm_bk(int bn) { return bn > 256 ? 32 : 64; }
+int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
+
+int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
+  const int bk = gemm_bk(bn);
+  int rc = make_tmap_bf16_2d(&m->a, A, K, M, K, bk, 128, 2 * bk);
+  rc |= make_tmap_bf16_2d(&m->b, W, K, N, K, bk, gemm_b_box_rows(bn), 2 * bk);
+  return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
+}
+
+// Output map of a row-major bf16 [rows, cols] matrix for the 32-row x 64-column
+// epilogue chunks (128B swizzle).
+int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols) {
+  return make_tmap_bf16_2d(m, D, cols, rows, cols, 64, 32, 128);
+}
+
+// QKV outputs: Q, K [rows*H*T, 64] and V^T [rows*H*64, T] (32-token x 64-dim chunks, 64B swizzle).
+int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T) {
+  const int64_t bh = rows * heads;
+  int rc = make_tmap_bf16_2d(&m->d[0], q, 64, bh * T, 64, 64, 32, 128);
+  rc |= make_tmap_bf16_2d(&m->d[1], k, 64, bh * T, 64, 64, 32, 128);
+  rc |= make_tmap_bf16_2d(&m->d[2], vt, T, bh * 64, T, 32, 64, 64);
+  return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
+}
+
 template <int BN, int KIND>
 constexpr int epi_warps() {
-  return KIND == EPI_RES_LN || KIND == EPI_QKV ? 4 : 8;
+  return KIND == EPI_QKV ? 4 : 8;
 }
 
 template <int BN, int KIND>
@@ -81,26 +110,24 @@ static int sm_count() {
 }
 
 template <int BN, int KIND>
-static int launch_one(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, const EpiParams& ep,
-                      cudaStream_t st) {
+static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams& ep, cudaStream_t st) {
   constexpr int W = epi_warps<BN, KIND>();
   using C = GemmCfg<BN, W>;
+  if (K % C::BK) return SF_ERR_PARAMETER;
   if (set_attr<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
   const int tiles = (N / BN) * ((M + C::BM - 1) / C::BM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   EpiParams e = ep;
   e.M = M;
-  gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(a, b, N, K, e);
+  gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(maps, N, K, e);
   return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
 
-int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
-
-int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                const EpiParams& ep, cudaStream_t st) {
-  if (K % 64 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
+int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
+                cudaStream_t st) {
+  if (K % 32 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
 #define SF_CASE(BN_, KIND_) \
-  if (bn == BN_ && kind == KIND_) return launch_one<BN_, KIND_>(a, b, M, N, K, ep, st);
+  if (bn == BN_ && kind == KIND_) return launch_one<BN_, KIND_>(maps, M, N, K, ep, st);
   SF_CASE(128, EPI_F32)
   SF_CASE(128, EPI_BF16)
   SF_CASE(128, EPI_GELU)

@@ -12,7 +12,9 @@
 //                32*(w%4)..+31 (one accumulator row per thread), two warps per
 //                lane quarter split the columns when EPI_WARPS == 8
 // The accumulator is double-buffered in TMEM when 2*BN <= 512 columns, so the
-// epilogue of tile i overlaps the main loop of tile i+1.
+// epilogue of tile i overlaps the main loop of tile i+1.  Epilogue outputs are
+// staged per warp in 128B-swizzled smem (32 rows x 64 columns, double-buffered)
+// and written with TMA bulk stores, so HBM sees full-line writes.
 #pragma once
 #include "sf_ptx.cuh"
 
@@ -28,35 +30,41 @@ enum EpiKind : int {
 
 struct EpiParams {
   const float* bias;  // [N]
-  void* out;          // EPI_F32/BF16/GELU
+  void* out;          // EPI_F32 direct stores
   int64_t ldo;
   // EPI_QKV
-  __nv_bfloat16* q;
-  __nv_bfloat16* k;
-  __nv_bfloat16* vt;
   int heads;
   float q_scale;
   // EPI_RES_LN
-  __nv_bfloat16* xres;   // [M, N] residual stream, updated in place
-  __nv_bfloat16* xmod;   // [M, N] modulated LayerNorm output
-  const float* gate;     // per-slot vectors: ptr + slot * vec_stride
+  const __nv_bfloat16* xres;  // [M, N] residual stream (read; the update goes out through d[0])
+  const float* gate;          // per-slot vectors: ptr + slot * vec_stride
   const float* shift;
   const float* scale;
   int64_t vec_stride;
   float ln_eps;
   // common
-  int tokens_per_slot;   // rows of one latent (1024); tiles never straddle a slot
-  int M;                 // valid rows (tail rows of the last tile are masked)
+  int tokens_per_slot;  // rows of one latent (1024); tiles never straddle a slot
+  int M;                // valid rows (tail rows of the last tile are masked)
+  int no_store;         // diagnostics only: skip the epilogue's global stores
+};
+
+// TMA descriptors: A, B operands and up to three outputs
+//   BF16/GELU: d[0] = out [M, N]          (box 64 x 32, SW128)
+//   QKV:       d[0] = Q [R*H*T, 64], d[1] = K (box 64 x 32, SW128),
+//              d[2] = V^T [R*H*64, T]     (box 32 x 64, SW64)
+//   RES_LN:    d[0] = xres, d[1] = xmod [M, N] (box 64 x 32, SW128)
+struct GemmMaps {
+  CUtensorMap a, b, d[3];
 };
 
 template <int BN, int EPI_WARPS>
 struct GemmCfg {
   static constexpr int BM = 128;
-  static constexpr int BK = 64;  // 128 B of bf16 = one SW128 atom row
+  static constexpr int BK = BN > 256 ? 32 : 64;  // K elements per stage (64 B / 128 B rows)
+  static constexpr int SWZ = BK * 2;             // swizzle width of the operand tiles (bytes)
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int MMA_N = BN > 256 ? BN / 2 : BN;  // UMMA N <= 256
   static constexpr int N_SPLIT = BN / MMA_N;
   static constexpr int B_BOX = BN > 256 ? BN / 2 : BN;  // TMA box rows <= 256
@@ -64,7 +72,14 @@ struct GemmCfg {
   static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;  // column offset between accumulator stages
   static constexpr int TMEM_COLS = ACC_STAGES == 2 ? (BN <= 128 ? 256 : 512) : (BN <= 256 ? 256 : 512);
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr int RED_BYTES = 2 * 8 * 32 * 4;      // LN partial sums of paired epilogue warps
+  static constexpr int VEC_BYTES = 2 * 4 * BN * 4;      // per-tile column vectors, double-buffered
+  static constexpr int OUT_BYTES = EPI_WARPS * 2 * 4096;  // per-warp output staging, double-buffered
+  static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES;
+  static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int SMEM_BYTES = FIXED + STAGES * STAGE_BYTES;
+  static_assert(STAGES >= 3, "pipeline too shallow");
   static_assert(MMA_N % 16 == 0 && MMA_N <= 256, "bad MMA N");
   static_assert(B_BOX <= 256, "bad box");
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
@@ -82,16 +97,51 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* v) {
   return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
 }
 
+// K-major operand descriptor for a 64 B (SW64) or 128 B (SW128) swizzled tile.
+template <int SWZ>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t smem_addr) {
+  if constexpr (SWZ == 128) return sw128_kmajor_desc(smem_addr);
+  return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+// Per-warp output staging: a 32-row x 128-byte tile in the TMA 128B-swizzle
+// layout.  Lane = row; 16-byte chunk c of the row lives at chunk c ^ (row & 7).
+struct OutStage {
+  uint8_t* base;     // this warp's 2 x 4 KB
+  uint32_t count;    // chunks issued so far by this warp (buffer = count & 1)
+  __device__ __forceinline__ uint8_t* acquire(uint32_t lane) {
+    if (count >= 2 && lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago left this buffer
+    __syncwarp();
+    return base + (count & 1) * 4096;
+  }
+  __device__ __forceinline__ static void put16(uint8_t* buf, uint32_t row, uint32_t chunk, uint4 v) {
+    *reinterpret_cast<uint4*>(buf + row * 128 + ((chunk ^ (row & 7)) * 16)) = v;
+  }
+  __device__ __forceinline__ void release(uint32_t lane, const CUtensorMap* map, uint8_t* buf, int c0, int c1,
+                                          bool store) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (store) tma_store_2d(map, buf, c0, c1);
+      bulk_commit();
+    }
+    ++count;
+  }
+};
+
 template <int BN, int KIND, int EPI_WARPS>
 __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
-    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int N,
-                      int K, EpiParams ep) {
+    gemm_bf16_tcgen05(const __grid_constant__ GemmMaps maps, int N, int K, EpiParams ep) {
   using C = GemmCfg<BN, EPI_WARPS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sOut = smem;                             // [EPI_WARPS][2][4096]   (1024-aligned)
+  uint8_t* sA = sOut + C::OUT_BYTES;                // [STAGES][A_BYTES]
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;        // [STAGES][B_BYTES]
+  float* red = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);  // [2][8 warps][32]
+  float* vecs = red + C::RED_BYTES / 4;                                // [2][4][BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vecs + C::VEC_BYTES / 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -106,8 +156,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
   const int num_kb = K / C::BK;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    tma_prefetch(&maps.a);
+    tma_prefetch(&maps.b);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -134,10 +184,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
-          tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * C::BK, m0);
+          tma_load_2d(sA + s * C::A_BYTES, &maps.a, &full[s], kb * C::BK, m0);
 #pragma unroll
           for (int h = 0; h < BN / C::B_BOX; ++h)
-            tma_load_2d(sB + s * C::B_BYTES + h * C::B_BOX * 128, &tmB, &full[s], kb * C::BK, n0 + h * C::B_BOX);
+            tma_load_2d(sB + s * C::B_BYTES + h * C::B_BOX * C::SWZ, &maps.b, &full[s], kb * C::BK,
+                        n0 + h * C::B_BOX);
         }
       }
     }
@@ -161,8 +212,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           for (int k = 0; k < C::BK / 16; ++k) {
 #pragma unroll
             for (int h = 0; h < C::N_SPLIT; ++h)
-              mma_bf16_ss(d + h * C::MMA_N, sw128_kmajor_desc(a_addr + k * 32),
-                          sw128_kmajor_desc(b_addr + h * C::MMA_N * 128 + k * 32), idesc, (kb | k) != 0);
+              mma_bf16_ss(d + h * C::MMA_N, kmajor_desc<C::SWZ>(a_addr + k * 32),
+                          kmajor_desc<C::SWZ>(b_addr + h * C::MMA_N * C::SWZ + k * 32), idesc, (kb | k) != 0);
           }
           mma_commit(&empty[s]);
         }
@@ -173,140 +224,202 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     // ---------------- epilogue warps
     const uint32_t e = warp - 2;
     const uint32_t quarter = warp & 3;
+    constexpr int EPI_THREADS = EPI_WARPS * 32;
     constexpr int COLS = EPI_WARPS == 8 ? BN / 2 : BN;
     const int c_lo = EPI_WARPS == 8 ? (int)(e / 4) * COLS : 0;
+    const int et = threadIdx.x - 64;
+    OutStage out{sOut + e * 8192, 0};
+    const bool do_store = !ep.no_store;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
       const int m0 = (tile / num_n) * C::BM, n0 = (tile % num_n) * BN;
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
-      const int row = m0 + quarter * 32 + lane;
+      const int r0 = m0 + quarter * 32;  // first row of this warp
+      const int row = r0 + lane;
       const bool valid = row < ep.M;
       const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * C::ACC_STRIDE;
+      const int slot = m0 / ep.tokens_per_slot;
+      // Stage this tile's per-column vectors in smem (double-buffered by tile
+      // parity) and start the residual loads *before* waiting for the
+      // accumulator: their latency hides under the main loop.
+      float* vb = vecs + (local & 1) * (4 * BN);
+      for (int c = et; c < BN; c += EPI_THREADS) {
+        vb[c] = ep.bias[n0 + c];
+        if constexpr (KIND == EPI_RES_LN) {
+          const int64_t o = (int64_t)slot * ep.vec_stride + n0 + c;
+          vb[BN + c] = ep.gate[o];
+          vb[2 * BN + c] = ep.shift[o];
+          vb[3 * BN + c] = ep.scale[o];
+        }
+      }
+      constexpr int PF = 2;  // RES_LN: residual chunks (32 columns) in flight
+      uint4 old[KIND == EPI_RES_LN ? PF : 1][4];
+      const uint4* old_src = reinterpret_cast<const uint4*>(ep.xres + (int64_t)row * N + n0 + c_lo);
+      if constexpr (KIND == EPI_RES_LN) {
+#pragma unroll
+        for (int q = 0; q < PF; ++q)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) old[q][i] = valid ? old_src[4 * q + i] : make_uint4(0, 0, 0, 0);
+      }
+      named_bar_sync(5, EPI_THREADS);  // vectors staged
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      const float* vbias = vb + c_lo;
 
-      if constexpr (KIND == EPI_F32 || KIND == EPI_BF16 || KIND == EPI_GELU) {
+      if constexpr (KIND == EPI_F32) {
 #pragma unroll 1
-        for (int c0 = c_lo; c0 < c_lo + COLS; c0 += 32) {
+        for (int c0 = 0; c0 < COLS; c0 += 32) {
           float v[32];
-          tmem_ld32(taddr + c0, v);
+          tmem_ld32(taddr + c_lo + c0, v);
           tmem_ld_wait();
-          const float4* bp = reinterpret_cast<const float4*>(ep.bias + n0 + c0);
+          if (valid && do_store) {
+            float4* dst =
+                reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + n0 + c_lo + c0);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 b = __ldg(bp + i);
-            v[4 * i] += b.x;
-            v[4 * i + 1] += b.y;
-            v[4 * i + 2] += b.z;
-            v[4 * i + 3] += b.w;
-          }
-          if constexpr (KIND == EPI_GELU) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-          }
-          if (valid) {
-            if constexpr (KIND == EPI_F32) {
-              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + n0 + c0);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
-              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + (int64_t)row * ep.ldo + n0 + c0);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) dst[i] = pack8_bf16(v + 8 * i);
+            for (int i = 0; i < 8; ++i) {
+              const float4 b = reinterpret_cast<const float4*>(vbias + c0)[i];
+              dst[i] = make_float4(v[4 * i] + b.x, v[4 * i + 1] + b.y, v[4 * i + 2] + b.z, v[4 * i + 3] + b.w);
             }
           }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      } else if constexpr (KIND == EPI_BF16 || KIND == EPI_GELU) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < COLS; c0 += 64) {
+          uint8_t* buf = out.acquire(lane);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
+              v[4 * i] += b.x;
+              v[4 * i + 1] += b.y;
+              v[4 * i + 2] += b.z;
+              v[4 * i + 3] += b.w;
+            }
+            if constexpr (KIND == EPI_GELU) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, 4 * h + i, pack8_bf16(v + 8 * i));
+          }
+          if (c0 + 64 >= COLS) {  // last TMEM read of this tile by this warp
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_QKV) {
         // columns [0, d) -> Q, [d, 2d) -> K, [2d, 3d) -> V; 64 columns per head
         const int d = ep.heads * 64;
         const int T = ep.tokens_per_slot;
-        const int slot = m0 / T;
-        const int tok = row - slot * T;
+        const int tok0 = r0 - slot * T;
 #pragma unroll 1
-        for (int c0 = c_lo; c0 < c_lo + COLS; c0 += 64) {
-          const int gc = n0 + c0;
+        for (int c0 = 0; c0 < COLS; c0 += 64) {
+          const int gc = n0 + c_lo + c0;
           const int which = gc / d;
           const int head = (gc - which * d) / 64;
-          float v[64];
-          tmem_ld32(taddr + c0, *reinterpret_cast<float(*)[32]>(&v[0]));
-          tmem_ld32(taddr + c0 + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
-          tmem_ld_wait();
+          const int64_t hb = ((int64_t)slot * ep.heads + head);
           const float sc = which == 0 ? ep.q_scale : 1.0f;
-          const float4* bp = reinterpret_cast<const float4*>(ep.bias + gc);
+          uint8_t* buf = out.acquire(lane);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float4 b = __ldg(bp + i);
-            v[4 * i] = (v[4 * i] + b.x) * sc;
-            v[4 * i + 1] = (v[4 * i + 1] + b.y) * sc;
-            v[4 * i + 2] = (v[4 * i + 2] + b.z) * sc;
-            v[4 * i + 3] = (v[4 * i + 3] + b.w) * sc;
-          }
-          if (valid) {
-            const int64_t hb = ((int64_t)slot * ep.heads + head);
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
+              v[4 * i] = (v[4 * i] + b.x) * sc;
+              v[4 * i + 1] = (v[4 * i + 1] + b.y) * sc;
+              v[4 * i + 2] = (v[4 * i + 2] + b.z) * sc;
+              v[4 * i + 3] = (v[4 * i + 3] + b.w) * sc;
+            }
             if (which < 2) {
-              uint4* dst = reinterpret_cast<uint4*>((which == 0 ? ep.q : ep.k) + (hb * T + tok) * 64);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) dst[i] = pack8_bf16(v + 8 * i);
+              for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, 4 * h + i, pack8_bf16(v + 8 * i));
             } else {
-              __nv_bfloat16* base = ep.vt + hb * 64 * T + tok;
+              // V^T staging: 64 rows (head dim) x 64 B (32 tokens), 64B swizzle:
+              // 16-byte chunk c of row dd lives at chunk c ^ ((dd >> 1) & 3)
 #pragma unroll
-              for (int i = 0; i < 64; ++i) base[(int64_t)i * T] = __float2bfloat16_rn(v[i]);
+              for (int i = 0; i < 32; ++i) {
+                const uint32_t dd = 32 * h + i;
+                *reinterpret_cast<__nv_bfloat16*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
+                                                  (lane & 7) * 2) = __float2bfloat16_rn(v[i]);
+              }
             }
           }
+          if (c0 + 64 >= COLS) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          if (which < 2)
+            out.release(lane, &maps.d[which], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          else
+            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_RES_LN) {
-        static_assert(KIND != EPI_RES_LN || EPI_WARPS == 4, "RES_LN needs whole rows per thread");
-        const int slot = m0 / ep.tokens_per_slot;
-        const float* gate = ep.gate + (int64_t)slot * ep.vec_stride + n0;
-        const float* shift = ep.shift + (int64_t)slot * ep.vec_stride + n0;
-        const float* scale = ep.scale + (int64_t)slot * ep.vec_stride + n0;
-        // pass 1: residual update, write bf16 residual, keep fp32 copy in TMEM, row sum
+        static_assert(KIND != EPI_RES_LN || (EPI_WARPS == 8 && COLS % 64 == 0), "RES_LN pairs two warps per row");
+        const float* vgate = vb + BN + c_lo;
+        const float* vshift = vb + 2 * BN + c_lo;
+        const float* vscale = vb + 3 * BN + c_lo;
+        const uint32_t tcol = taddr + c_lo;
+        const bool st_ok = do_store && r0 < ep.M;
+        // pass 1: x_new = x + gate*(acc + bias) -> bf16 residual (TMA store) and its
+        // rounded fp32 value back into TMEM; partial row sum over this half
         float sum = 0.f;
-        __nv_bfloat16* xr = ep.xres + (int64_t)row * N + n0;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint8_t* buf = nullptr;
+#pragma unroll
+        for (int q = 0; q < COLS / 32; ++q) {
+          if ((q & 1) == 0) buf = out.acquire(lane);
           float v[32];
-          tmem_ld32(taddr + c0, v);
-          uint4 old[4];
-          if (valid) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) old[i] = reinterpret_cast<const uint4*>(xr + c0)[i];
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) old[i] = make_uint4(0, 0, 0, 0);
-          }
+          tmem_ld32(tcol + 32 * q, v);
           tmem_ld_wait();
+          uint4 cur[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) cur[i] = old[q % PF][i];
+          if (q + PF < COLS / 32) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) old[q % PF][i] = valid ? old_src[4 * (q + PF) + i] : make_uint4(0, 0, 0, 0);
+          }
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + c0) + i);
-            const float4 g = __ldg(reinterpret_cast<const float4*>(gate + c0) + i);
-            const float2 o0 = unpack_bf16(reinterpret_cast<const uint32_t*>(old)[2 * i]);
-            const float2 o1 = unpack_bf16(reinterpret_cast<const uint32_t*>(old)[2 * i + 1]);
-            packed[2 * i] = pack_bf16(o0.x + g.x * (v[4 * i] + b.x), o0.y + g.y * (v[4 * i + 1] + b.y));
-            packed[2 * i + 1] = pack_bf16(o1.x + g.z * (v[4 * i + 2] + b.z), o1.y + g.w * (v[4 * i + 3] + b.w));
-            const float2 r0 = unpack_bf16(packed[2 * i]), r1 = unpack_bf16(packed[2 * i + 1]);
-            v[4 * i] = r0.x;  // LayerNorm sees the stored (rounded) residual
-            v[4 * i + 1] = r0.y;
-            v[4 * i + 2] = r1.x;
-            v[4 * i + 3] = r1.y;
-            sum += (r0.x + r0.y) + (r1.x + r1.y);
+            const float4 bb = reinterpret_cast<const float4*>(vbias + 32 * q)[i];
+            const float4 g = reinterpret_cast<const float4*>(vgate + 32 * q)[i];
+            const uint32_t* ow = reinterpret_cast<const uint32_t*>(cur);
+            const float2 o0 = unpack_bf16(ow[2 * i]), o1 = unpack_bf16(ow[2 * i + 1]);
+            packed[2 * i] = pack_bf16(o0.x + g.x * (v[4 * i] + bb.x), o0.y + g.y * (v[4 * i + 1] + bb.y));
+            packed[2 * i + 1] = pack_bf16(o1.x + g.z * (v[4 * i + 2] + bb.z), o1.y + g.w * (v[4 * i + 3] + bb.w));
+            const float2 r0v = unpack_bf16(packed[2 * i]), r1v = unpack_bf16(packed[2 * i + 1]);
+            v[4 * i] = r0v.x;  // LayerNorm sees the stored (rounded) residual
+            v[4 * i + 1] = r0v.y;
+            v[4 * i + 2] = r1v.x;
+            v[4 * i + 3] = r1v.y;
+            sum += (r0v.x + r0v.y) + (r1v.x + r1v.y);
           }
-          if (valid) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              reinterpret_cast<uint4*>(xr + c0)[i] =
-                  make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-          }
-          tmem_st32(taddr + c0, v);
+          for (int i = 0; i < 4; ++i)
+            OutStage::put16(buf, lane, 4 * (q & 1) + i,
+                            make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]));
+          if (q & 1) out.release(lane, &maps.d[0], buf, n0 + c_lo + 32 * (q - 1), r0, st_ok);
+          tmem_st32(tcol + 32 * q, v);
         }
         tmem_st_wait();
-        const float mean = sum * (1.0f / BN);
+        // the two warps of this lane quarter hold the two halves of each row
+        red[e * 32 + lane] = sum;
+        named_bar_sync(1 + quarter, 64);
+        const float mean = (sum + red[(e ^ 4) * 32 + lane]) * (1.0f / N);
         float var = 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int q = 0; q < COLS / 32; ++q) {
           float v[32];
-          tmem_ld32(taddr + c0, v);
+          tmem_ld32(tcol + 32 * q, v);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -314,40 +427,40 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
             var += dlt * dlt;
           }
         }
-        const float rstd = rsqrtf(var * (1.0f / BN) + ep.ln_eps);
-        __nv_bfloat16* xm = ep.xmod + (int64_t)row * N + n0;
+        red[256 + e * 32 + lane] = var;
+        named_bar_sync(1 + quarter, 64);
+        const float rstd = rsqrtf((var + red[256 + (e ^ 4) * 32 + lane]) * (1.0f / N) + ep.ln_eps);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int q = 0; q < COLS / 32; ++q) {
+          if ((q & 1) == 0) buf = out.acquire(lane);
           float v[32];
-          tmem_ld32(taddr + c0, v);
+          tmem_ld32(tcol + 32 * q, v);
           tmem_ld_wait();
-          if (c0 + 32 == BN) {  // last TMEM read of this tile: hand the accumulator back early
+          if (q + 1 == COLS / 32) {  // last TMEM read of this tile: hand the accumulator back early
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
           }
-          uint32_t packed[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 sh = __ldg(reinterpret_cast<const float4*>(shift + c0) + i);
-            const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c0) + i);
-            packed[2 * i] = pack_bf16((v[4 * i] - mean) * rstd * (1.0f + sc.x) + sh.x,
-                                      (v[4 * i + 1] - mean) * rstd * (1.0f + sc.y) + sh.y);
-            packed[2 * i + 1] = pack_bf16((v[4 * i + 2] - mean) * rstd * (1.0f + sc.z) + sh.z,
-                                          (v[4 * i + 3] - mean) * rstd * (1.0f + sc.w) + sh.w);
-          }
-          if (valid) {
+          for (int i = 0; i < 4; ++i) {
+            float o[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              reinterpret_cast<uint4*>(xm + c0)[i] =
-                  make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            for (int k = 0; k < 2; ++k) {
+              const float4 sh = reinterpret_cast<const float4*>(vshift + 32 * q)[2 * i + k];
+              const float4 sc = reinterpret_cast<const float4*>(vscale + 32 * q)[2 * i + k];
+              const float* vv = v + 8 * i + 4 * k;
+              o[4 * k] = (vv[0] - mean) * rstd * (1.0f + sc.x) + sh.x;
+              o[4 * k + 1] = (vv[1] - mean) * rstd * (1.0f + sc.y) + sh.y;
+              o[4 * k + 2] = (vv[2] - mean) * rstd * (1.0f + sc.z) + sh.z;
+              o[4 * k + 3] = (vv[3] - mean) * rstd * (1.0f + sc.w) + sh.w;
+            }
+            OutStage::put16(buf, lane, 4 * (q & 1) + i, pack8_bf16(o));
           }
+          if (q & 1) out.release(lane, &maps.d[1], buf, n0 + c_lo + 32 * (q - 1), r0, st_ok);
         }
       }
-      if constexpr (KIND != EPI_RES_LN) {
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-      }
     }
+    if (lane == 0) bulk_wait<0>();  // all output stores of this warp have landed
+    __syncwarp();
   }
 
   tc_fence_before();

@@ -8,13 +8,18 @@
 
 namespace sf {
 struct EpiParams;
+struct GemmMaps;
 int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
-                      uint32_t box_inner, uint32_t box_outer);
+                      uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128);
+int gemm_bk(int bn);
 int gemm_b_box_rows(int bn);
+int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn);
+int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
+int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T);
 int prepare_gemm_kernels();
 int prepare_attn_kernel();
-int launch_gemm(int kind, int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                const EpiParams& ep, cudaStream_t st);
+int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
+                cudaStream_t st);
 
 struct AttnMaps {
   CUtensorMap q, k, v;
