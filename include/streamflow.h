@@ -143,8 +143,8 @@ int sf_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, int x_dtype, 
 int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
                  int32_t epi, void* stream);
 
-/* QKV projection with head-major scatter: Q, K -> [M/T, heads, T, 64] (Q
- * multiplied by q_scale), V -> V^T [M/T, heads, 64, T].  K = heads*64. */
+/* QKV projection with head-major scatter: Q, K -> [M/T, heads, T, 64] bf16 (Q
+ * multiplied by q_scale), V -> V^T [M/T, heads, 64, T] fp16.  K = heads*64. */
 int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,
                 int32_t T, float q_scale, void* stream);
 
@@ -157,8 +157,8 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream);
 
-/* K6 -- flash attention, T tokens per row, head dim 64, no mask.
- * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T];
+/* K6 -- flash attention, T tokens per row (multiple of 256), head dim 64, no mask.
+ * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T] fp16;
  * out: [rows * T, heads * 64] bf16 (token-major, heads concatenated). */
 int sf_attention(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads, int32_t T,
                  void* stream);

@@ -13,7 +13,7 @@ import re
 from .errors import InvariantError, ParameterError, StateError, TimeDomainError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstreamflow.so")
+LIB_PATH = os.environ.get("SF_LIB_PATH") or os.path.join(_HERE, "libstreamflow.so")  # override: diagnostics
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "streamflow.h")
 
 SF_OK = 0

@@ -24,7 +24,7 @@ enum EpiKind : int {
   EPI_F32 = 0,     // out f32 [M, ldo]  = acc + bias
   EPI_BF16 = 1,    // out bf16 [M, ldo] = acc + bias
   EPI_GELU = 2,    // out bf16 [M, ldo] = gelu_tanh(acc + bias)
-  EPI_QKV = 3,     // scatter to Q,K [rows, H, T, 64] and V^T [rows, H, 64, T]; Q pre-scaled
+  EPI_QKV = 3,     // scatter to Q,K [rows, H, T, 64] bf16 and V^T [rows, H, 64, T] fp16; Q pre-scaled
   EPI_RES_LN = 4,  // x += gate*(acc+bias) (bf16 residual); xmod = LN(x)*(1+scale)+shift
 };
 
@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const uint32_t dd = 32 * h + i;
-                *reinterpret_cast<__nv_bfloat16*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
-                                                  (lane & 7) * 2) = __float2bfloat16_rn(v[i]);
+                *reinterpret_cast<__half*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
+                                           (lane & 7) * 2) = __float2half_rn(v[i]);  // V^T is fp16 (PV runs in fp16)
               }
             }
           }

@@ -2,8 +2,10 @@
 // Everything here is written directly against the PTX ISA; no CUTLASS/CuTe.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace sf {
@@ -41,15 +43,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug becomes a reported device fault (trap) instead
+// of a hung GPU.  2^28 polls is far beyond any legitimate wait (seconds).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  for (uint32_t n = 0;; ++n) {
+    if (mbar_try_wait(addr, parity)) return;
+    if (n > (1u << 28)) {
+      printf("streamflow: mbarrier wait timeout (block %d thread %d, smem 0x%x, parity %u)\n", (int)blockIdx.x,
+             (int)threadIdx.x, addr, parity);
+      asm volatile("trap;");
+    }
+  }
 }
 
 // ---------------------------------------------------------------- TMA

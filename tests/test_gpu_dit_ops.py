@@ -34,7 +34,7 @@ def test_qkv_scatter(rows):
     b = torch.randn(3 * d, device="cuda", generator=g) * 0.1
     q = torch.empty(rows, H, T, 64, device="cuda", dtype=torch.bfloat16)
     k = torch.empty_like(q)
-    vt = torch.empty(rows, H, 64, T, device="cuda", dtype=torch.bfloat16)
+    vt = torch.empty(rows, H, 64, T, device="cuda", dtype=torch.float16)
     L().call("sf_gemm_qkv", a.data_ptr(), w.data_ptr(), b.data_ptr(), q.data_ptr(), k.data_ptr(),
              vt.data_ptr(), M, H, T, 0.125, st())
     torch.cuda.synchronize()
@@ -79,7 +79,7 @@ def test_attention_matches_sdpa(rows, H, scale):
     q = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g) * scale / 8)
     k = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g))
     v = bf(torch.randn(rows, H, T, 64, device="cuda", generator=g))
-    vt = v.transpose(-1, -2).contiguous()
+    vt = v.transpose(-1, -2).contiguous().to(torch.float16)  # PV runs in fp16
     out = torch.empty(rows * T, H * 64, device="cuda", dtype=torch.bfloat16)
     L().call("sf_attention", q.data_ptr(), k.data_ptr(), vt.data_ptr(), out.data_ptr(), rows, H, T, st())
     torch.cuda.synchronize()
