@@ -1,130 +1,203 @@
 // Flash attention for the DiT velocity field on tcgen05 / TMEM / TMA (sm_100a).
 //
-// One CTA = one (latent row, head) pair x TWO 128-query tiles (A, B) that
-// ping-pong on the tensor core; T tokens (1024), head dim 64, no mask.  Q
-// arrives pre-scaled by 1/sqrt(64) from the QKV GEMM epilogue and V arrives
-// transposed ([hd, T]) so every MMA reads K-major operands.  KV tiles are 64
-// keys wide.
+// Persistent kernel: one CTA per SM walks work items (latent row, head, pair of
+// 128-query tiles A/B); T tokens (1024), head dim 64, no mask.  Q arrives
+// pre-scaled by 1/sqrt(64) from the QKV GEMM epilogue, V arrives transposed
+// ([hd, T], fp16) so every MMA reads K-major operands.  KV tiles are 64 keys.
 //
-//   warps 0-3   softmax of tile A (thread r = query row r)
+//   warps 0-3   softmax of tile A (thread r = query row r = TMEM lane r)
 //   warps 4-7   softmax of tile B
-//   warp 8      TMA producer: Q_A, Q_B once; K_j / V_j^T into a 6-stage ring
-//   warps 9,10  MMA issuers, one per query tile (warp 9 also owns TMEM), so the
-//               two tiles progress independently
-//                 S_t[j%2] = Q_t . K_j^T   (M=128, N=64, K=64)
-//                 O_t     += P_t . V_j     (M=128, N=64, K=64)
-// TMEM columns: S_A0 [0,64) S_A1 [64,128) S_B0 [128,192) S_B1 [192,256)
-//               O_A [256,320) O_B [320,384).
+//   warp 8      TMA producer: Q (double-buffered across items), K_j / V_j^T ring
+//   warps 9,10  MMA issuers, one per query tile (warp 9 owns TMEM)
 //
-// S and P are double-buffered per tile and S is issued two KV tiles ahead, so
-// a softmax warp finds its scores ready and never waits for the PV of the
-// previous tile; each S buffer is released (s_free) as soon as the softmax has
-// the 64-wide score row in registers, so S two tiles ahead overlaps the exp.
-// Softmax per KV tile: tree max, P = exp2(s*log2e - m) -> fp16 -> 128B-swizzled
-// smem (A operand of the fp16 PV MMA); the row sum l comes out of the PV MMA as
-// column 64 of O (V^T carries a ones-row).  The O accumulator stays in TMEM and
-// the exponent reference m is updated lazily: only when a row max exceeds it by
-// more than 8 (log2 units, i.e. P <= 256) does the warp wait for the in-flight
-// PV and rescale its O rows in place (tcgen05.ld/st) -- exact, since l uses
-// the same reference.
+// TMEM (512 columns): S_A0 [0,64) S_A1 [64,128) S_B0 [128,192) S_B1 [192,256)
+//                     O_A [256,336) O_B [384,464)
+// S is double-buffered per tile; P_t(j) (fp16 pairs) is written by the softmax
+// into the upper 32 columns of S_t(j)'s buffer and consumed from TMEM by the PV
+// MMA (A operand in TMEM, "TS" form), so P never touches shared memory.  Per
+// tile t the tensor-core program is
+//     S_t(j) = Q_t K_j^T        (M=128, N=64, K=64, bf16 -> f32)
+//     O_t   += P_t(j) V_j       (M=128, N=80, K=64, fp16 -> f32; A from TMEM)
+// with S_t(j+2) issued right after PV_t(j) into the same buffer (tcgen05 MMAs of
+// one thread execute in issue order, so S_t(j+2) cannot overwrite P_t(j) before
+// PV_t(j) has read it); S is therefore computed a full softmax iteration ahead.
+// V^T carries a ones-row (row 64) so column 64 of O is the softmax row sum l of
+// exactly the fp16 P the MMA consumed.  The exponent reference m is updated
+// lazily (only when a row max grows by > 8 in log2 units; then the softmax
+// rescales O in TMEM).  Exponentials: a fixed share of each row goes through a
+// degree-3 polynomial 2^x on the FMA pipe (packed f32x2 ops), the rest through
+// MUFU.EX2.  Across items the MMA warps start S(0), S(1) of the next item right
+// after the last PVs of the current one and the producer prefetches the next Q,
+// so CTA prologues are hidden.
 #include "sf_internal.h"
 #include "sf_ptx.cuh"
 
-#ifndef SF_ATTN_SFREE
-#define SF_ATTN_SFREE 1  // release S buffers right after the score load
+#ifndef SF_ATTN_SAFE_S
+#define SF_ATTN_SAFE_S 0  // diagnostics: wait for PV_t(j) before S_t(j+2) reuses its buffer
 #endif
-#ifndef SF_ATTN_F16PV
-#define SF_ATTN_F16PV 1  // fp16 P/V^T with the ones-row row sum
+#ifndef SF_ATTN_DESYNC
+#define SF_ATTN_DESYNC 0
+#endif
+#ifndef SF_ATTN_TRACE
+#define SF_ATTN_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_attn_trace_read)
+#endif
+#ifndef SF_ATTN_EMU_PAIRS
+#define SF_ATTN_EMU_PAIRS 6  // exp2 pairs per 32-key chunk evaluated by polynomial (of 16)
 #endif
 
 namespace sf {
 
+#if SF_ATTN_TRACE
+__device__ long long g_attn_trace[8 * 64];
+#define ATR(role, idx)                                                               \
+  do {                                                                               \
+    if (blockIdx.x == 0 && (idx) < 64) g_attn_trace[(role) * 64 + (idx)] = clock64(); \
+  } while (0)
+#else
+#define ATR(role, idx) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace attn {
-constexpr int BQ = 128;  // queries per tile (2 tiles per CTA)
+constexpr int BQ = 128;  // queries per tile (2 tiles per item)
 constexpr int BKV = 64;  // keys per KV tile
 constexpr int HD = 64;
-constexpr int Q_BYTES = BQ * HD * 2;   // 16 KB per tile
-constexpr int K_BYTES = BKV * HD * 2;  // 8 KB  (64 kv rows x 128 B)
-constexpr int V_ROWS = HD + 16;        // V^T rows 0..63 from TMA; row 64 = ones (-> row sum l), 65..79 = 0
-constexpr int V_TMA_BYTES = HD * BKV * 2;   // 8 KB loaded per stage
-constexpr int V_BYTES = V_ROWS * BKV * 2;   // 10 KB per stage
-constexpr int P_BYTES = BQ * BKV * 2;  // 16 KB per tile and buffer (128 rows x 128 B)
-constexpr int KV_STAGES = 6;  // refill of tile j+6 starts after tile j: 3 iterations of slack
-constexpr int SMEM = 1024 + 2 * Q_BYTES + KV_STAGES * (K_BYTES + V_BYTES) + 4 * P_BYTES + 256;
-constexpr float RESCALE_LOG2 = 8.0f;  // lazy-rescale threshold
+constexpr int Q_TILE = BQ * HD * 2;    // 16 KB
+constexpr int Q_BYTES = 2 * Q_TILE;    // both tiles of an item
+constexpr int K_BYTES = BKV * HD * 2;  // 8 KB (64 kv rows x 128 B)
+constexpr int V_ROWS = HD + 16;        // V^T rows 0..63 from TMA; row 64 = ones (-> l), 65..79 = 0
+constexpr int V_BYTES = V_ROWS * 128;  // 80 rows x 128 B (SW128)
+constexpr int V_TMA = HD * 128;        // bytes loaded per stage
+constexpr int STAGE = K_BYTES + V_BYTES;
+constexpr int KV_STAGES = 6;
+constexpr int QBUF = 2;
+constexpr int SMEM = 1024 + QBUF * Q_BYTES + KV_STAGES * STAGE + 256;
+constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int TMEM_COLS = 512;
+// S_t,b: tile t, buffer b (64 fp32 columns); P_t,b (fp16 pairs) aliases its upper 32 columns
 __host__ __device__ constexpr uint32_t S_COL(int t, int b) { return 64u * (2 * t + b); }
-__host__ __device__ constexpr uint32_t O_COL(int t) { return 256u + 96u * t; }  // 80 used (64 O + l), 96 apart
-constexpr int THREADS = 352;  // 8 softmax warps + TMA warp + one MMA warp per tile
+__host__ __device__ constexpr uint32_t P_COL(int t, int b) { return 64u * (2 * t + b) + 32u; }
+__host__ __device__ constexpr uint32_t O_COL(int t) { return 256u + 128u * t; }
+constexpr int THREADS = 352;
 }  // namespace attn
-
-// exp2 of two fp32 arguments via one f16x2 MUFU op; returns the packed f16 pair
-// (lo = first argument), i.e. the P words for the fp16 PV MMA.
-__device__ __forceinline__ uint32_t ex2_f16x2(float lo, float hi) {
-  uint32_t x, y;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(x) : "f"(hi), "f"(lo));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// 2^x for a pair, on the FMA pipe: x = j + f (j = rint(x), |f| <= 1/2),
+// 2^f by a degree-3 minimax polynomial (rel. err 7.7e-5 < half an fp16 ulp),
+// 2^j added into the exponent field.  x is clamped to >= -127 (P underflows to 0 in fp16 anyway).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float kMagic = 12582912.0f;  // 1.5 * 2^23: x + magic rounds x to an integer in the low mantissa bits
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+  const float2 jf = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+  const float2 f = __ffma2_rn(jf, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(f, make_float2(0.055088773f, 0.055088773f), make_float2(0.24260406f, 0.24260406f));
+  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
+  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  const uint32_t b0 = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t b1 = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(b0), __uint_as_float(b1));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  tmem_st16u(taddr, *reinterpret_cast<const uint32_t(*)[16]>(&v[0]));
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T (A operand read from TMEM, "TS" form).
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 __global__ void __launch_bounds__(attn::THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int T, int heads) {
+                     const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int T, int heads,
+                     int nitems) {
   using namespace attn;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                      // [2][Q_BYTES]
-  uint8_t* sK = sQ + 2 * Q_BYTES;          // [KV_STAGES][K_BYTES]
-  uint8_t* sV = sK + KV_STAGES * K_BYTES;  // [KV_STAGES][V_BYTES]
-  uint8_t* sP = sV + KV_STAGES * V_BYTES;  // [tile][buffer][P_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * P_BYTES);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;                 // [KV_STAGES]
-  uint64_t* kv_empty = bars + 1 + KV_STAGES;    // [KV_STAGES]
-  uint64_t* s_full = bars + 1 + 2 * KV_STAGES;  // [tile][buffer] = 4
-  // [tile][P buffer]: P written, S buffer consumed, O rescaled.  One barrier per
-  // buffer: a softmax warpgroup may run a full tile ahead of the MMA thread, and
-  // per-buffer phases can never be lapped (tile j+2 needs S issued after tile j).
-  uint64_t* p_full = s_full + 4;
-  uint64_t* o_full = p_full + 4;                // [tile][P buffer]: PV that read that buffer is done
-  uint64_t* s_free = o_full + 4;                // [tile][S buffer]: scores copied to registers
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 4);
-  static_assert(8 * (1 + 2 * KV_STAGES + 4 + 4 + 4 + 4) + 4 <= 256, "barrier area");
+  uint8_t* sQ = smem;                  // [QBUF][2 tiles][Q_TILE]
+  uint8_t* sKV = sQ + QBUF * Q_BYTES;  // [KV_STAGES][K (64 x 128 B) | V^T (80 x 128 B)]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + KV_STAGES * STAGE);
+  uint64_t* q_full = bars;                   // [QBUF]
+  uint64_t* q_empty = bars + 2;              // [QBUF]   both tiles issued their last S on this Q
+  uint64_t* kv_full = bars + 4;              // [KV_STAGES]
+  uint64_t* kv_empty = kv_full + KV_STAGES;  // [KV_STAGES]  both tiles' PV on this K/V done
+  uint64_t* s_full = kv_empty + KV_STAGES;   // [tile][buffer]  S_t(j) landed in TMEM
+  uint64_t* p_full = s_full + 4;             // [tile][buffer]  P_t(j) written to TMEM (O rescaled if needed)
+  // [tile][buffer]  PV_t(j) complete.  Per buffer so that a wait is never two
+  // phases behind: when softmax(j) runs, PV_t(j-2) is known complete (S_t(j)
+  // was issued after it) but PV_t(j-1) need not be.
+  uint64_t* o_full = p_full + 4;
+  uint64_t* o_free = o_full + 4;             // [tile]  epilogue has read O_t
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+  static_assert(8 * (4 + 2 * KV_STAGES + 14) + 4 <= 256, "barrier area");
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int q0 = blockIdx.x * (2 * BQ);
-  const int bh = blockIdx.y;  // row * heads + head
-  const int nkv = T / BKV;
+  const int nkv = T / BKV;  // even (T % 256 == 0): buffer of global KV iteration G is G & 1
+  const int qpairs = T / (2 * BQ);
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
+    for (int i = 0; i < QBUF; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 2);
+    }
     for (int s = 0; s < KV_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 2);  // released by both MMA issuers
+      mbar_init(&kv_empty[s], 2);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 128);
-    for (int i = 0; i < 4; ++i) mbar_init(&o_full[i], 1);
-    for (int i = 0; i < 4; ++i) mbar_init(&s_free[i], 128);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_full[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], 128);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<TMEM_COLS>(tmem_holder);
   // V^T rows 64..79 of every stage: row 64 = fp16 ones (its PV output column is
-  // the softmax row sum), rows 65..79 = 0.  Constant rows are swizzle-invariant.
+  // the softmax row sum), rows 65..79 = 0 (constant rows are swizzle-invariant).
   for (int i = threadIdx.x; i < KV_STAGES * 16 * 8; i += blockDim.x) {
     const int stg = i / 128, rr = i % 128 / 8, ch = i % 8;
     const uint32_t w = rr == 0 ? 0x3C003C00u : 0u;
-    *reinterpret_cast<uint4*>(sV + stg * V_BYTES + (HD + rr) * 128 + ch * 16) = make_uint4(w, w, w, w);
+    *reinterpret_cast<uint4*>(sKV + stg * STAGE + K_BYTES + (HD + rr) * 128 + ch * 16) = make_uint4(w, w, w, w);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -135,76 +208,89 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
   if (warp == 8) {
     if (lane == 0) {
       // ---------------- TMA producer
-      mbar_expect_tx(q_full, 2 * Q_BYTES);
-      tma_load_2d(sQ, &tmQ, q_full, 0, bh * T + q0);
-      tma_load_2d(sQ + Q_BYTES, &tmQ, q_full, 0, bh * T + q0 + BQ);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % KV_STAGES;
-        mbar_wait(&kv_empty[s], ((j / KV_STAGES) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[s], K_BYTES + V_TMA_BYTES);
-        tma_load_2d(sK + s * K_BYTES, &tmK, &kv_full[s], 0, bh * T + j * BKV);
-        tma_load_2d(sV + s * V_BYTES, &tmV, &kv_full[s], j * BKV, bh * HD);
+      int kv = 0, local = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
+        const int bh = item / qpairs, q0 = (item % qpairs) * 2 * BQ;
+        const int qb = local & 1;
+        mbar_wait(&q_empty[qb], ((local >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], Q_BYTES);
+        tma_load_2d(sQ + qb * Q_BYTES, &tmQ, &q_full[qb], 0, bh * T + q0);
+        tma_load_2d(sQ + qb * Q_BYTES + Q_TILE, &tmQ, &q_full[qb], 0, bh * T + q0 + BQ);
+        for (int j = 0; j < nkv; ++j, ++kv) {
+          const int s = kv % KV_STAGES;
+          mbar_wait(&kv_empty[s], ((kv / KV_STAGES) & 1) ^ 1);
+          uint8_t* st = sKV + s * STAGE;
+          mbar_expect_tx(&kv_full[s], K_BYTES + V_TMA);
+          tma_load_2d(st, &tmK, &kv_full[s], 0, bh * T + j * BKV);
+          tma_load_2d(st + K_BYTES, &tmV, &kv_full[s], j * BKV, bh * HD);
+        }
       }
     }
   } else if (warp == 9 || warp == 10) {
     if (lane == 0) {
-      const int t = warp - 9;  // the query tile this thread issues for
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(128, 64);  // S = Q K^T: bf16, 128 x 64
-      // O = P V: fp16 P and V^T, 128 x 80 (the extra ones-row of V^T yields the row sum)
-#if SF_ATTN_F16PV
-      constexpr uint32_t idesc_pv = (1u << 4) | ((uint32_t)V_ROWS >> 3 << 17) | ((128u >> 4) << 24);
-#else
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 64);
-#endif
-      auto issue_s = [&](int t, int j) {
-        const uint32_t q_addr = smem_u32(sQ + t * Q_BYTES);
-        const uint32_t k_addr = smem_u32(sK + (j % KV_STAGES) * K_BYTES);
+      // ---------------- MMA issuer, one per query tile (the two progress independently)
+      const int t = warp - 9;
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, BKV);
+      constexpr uint32_t idesc_pv = (1u << 4) | ((uint32_t)V_ROWS >> 3 << 17) | ((128u >> 4) << 24);  // f16 A/B
+      auto issue_s = [&](int qb, int s, int b) {
+        const uint32_t q_addr = smem_u32(sQ + qb * Q_BYTES + t * Q_TILE);
+        const uint32_t k_addr = smem_u32(sKV + s * STAGE);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          mma_bf16_ss(tmem + S_COL(t, j & 1), sw128_kmajor_desc(q_addr + k * 32),
-                      sw128_kmajor_desc(k_addr + k * 32), idesc, k != 0);
-        mma_commit(&s_full[2 * t + (j & 1)]);
+          mma_bf16_ss(tmem + S_COL(t, b), sw128_kmajor_desc(q_addr + k * 32), sw128_kmajor_desc(k_addr + k * 32),
+                      idesc_s, k != 0);
+        mma_commit(&s_full[2 * t + b]);
       };
-      auto issue_pv = [&](int t, int j) {
-        const uint32_t p_addr = smem_u32(sP + (2 * t + (j & 1)) * P_BYTES);
-        const uint32_t v_addr = smem_u32(sV + (j % KV_STAGES) * V_BYTES);
+      auto issue_pv = [&](int s, int b, bool acc) {
+        const uint32_t v_addr = smem_u32(sKV + s * STAGE + K_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          mma_bf16_ss(tmem + O_COL(t), sw128_kmajor_desc(p_addr + k * 32), sw128_kmajor_desc(v_addr + k * 32),
-                      idesc_pv, (j | k) != 0);
-        mma_commit(&o_full[2 * t + (j & 1)]);
+          mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, sw128_kmajor_desc(v_addr + k * 32), idesc_pv,
+                     acc || k != 0);
+        mma_commit(&o_full[2 * t + b]);
       };
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < 2 && j < nkv; ++j) {
-        mbar_wait(&kv_full[j % KV_STAGES], (j / KV_STAGES) & 1);
-        tc_fence_after();
-        issue_s(t, j);
-      }
-#pragma unroll 1
-      for (int j = 0; j < nkv; ++j) {
-#if SF_ATTN_SFREE
-        if (j + 2 < nkv) {
-          // S buffer j%2 is free as soon as the softmax has the scores in registers
-          mbar_wait(&kv_full[(j + 2) % KV_STAGES], ((j + 2) / KV_STAGES) & 1);
-          mbar_wait(&s_free[2 * t + (j & 1)], (j >> 1) & 1);
-          tc_fence_after();
-          issue_s(t, j + 2);
-        }
-        mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);  // P_t(j) written, O_t rescaled
-        tc_fence_after();
-        issue_pv(t, j);
-#else
-        if (j + 2 < nkv) mbar_wait(&kv_full[(j + 2) % KV_STAGES], ((j + 2) / KV_STAGES) & 1);
-        mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);
-        tc_fence_after();
-        issue_pv(t, j);
-        if (j + 2 < nkv) issue_s(t, j + 2);
+      int kv = 0, local = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
+        const int qb = local & 1;
+        mbar_wait(&q_full[qb], (local >> 1) & 1);
+#if SF_ATTN_SAFE_S
+        if (kv > 0) mbar_wait(&o_full[2 * t + 1], ((kv - 1) >> 1) & 1);
 #endif
-        mma_commit(&kv_empty[j % KV_STAGES]);  // this tile is done with K_j / V_j
+#if SF_ATTN_DESYNC
+        // start tile B half a softmax behind tile A so their latency phases interleave
+        if (t == 1 && kv == 0) mbar_wait(&s_full[0], 0);
+#endif
+        for (int j = 0; j < 2; ++j) {
+          const int G = kv + j;
+          mbar_wait(&kv_full[G % KV_STAGES], (G / KV_STAGES) & 1);
+          tc_fence_after();
+          issue_s(qb, G % KV_STAGES, j);
+        }
+#pragma unroll 1
+        for (int j = 0; j < nkv; ++j) {
+          const int G = kv + j, b = j & 1;
+          mbar_wait(&p_full[2 * t + b], (G >> 1) & 1);          // P_t(j) in TMEM, O_t rescaled
+          ATR(4 + 2 * t, G);
+          if (j == 0) mbar_wait(&o_free[t], (local & 1) ^ 1);  // previous item's O read out
+          tc_fence_after();
+          issue_pv(G % KV_STAGES, b, j != 0);
+          mma_commit(&kv_empty[G % KV_STAGES]);
+          if (j + 2 < nkv) {
+            // S_t(j+2) reuses buffer b: issued after PV_t(j), which reads P_t(j) from it
+            mbar_wait(&kv_full[(G + 2) % KV_STAGES], ((G + 2) / KV_STAGES) & 1);
+#if SF_ATTN_SAFE_S
+            mbar_wait(&o_full[2 * t + b], (G >> 1) & 1);
+#endif
+            tc_fence_after();
+            ATR(5 + 2 * t, G + 2);
+            issue_s(qb, (G + 2) % KV_STAGES, b);
+            if (j + 3 == nkv) mma_commit(&q_empty[qb]);  // last S of this tile on this Q
+          }
+        }
+        kv += nkv;
       }
     }
-  } else if (warp < 8) {
+  } else {
     // ---------------- softmax warpgroups: warps 0-3 -> tile A, 4-7 -> tile B
     const int t = warp >> 2;
     const uint32_t quarter = warp & 3;
@@ -212,96 +298,91 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     const uint32_t lane_base = tmem + ((quarter * 32) << 16);
     const uint32_t o_addr = lane_base + O_COL(t);
     const float L2E = 1.4426950408889634f;
-    float m_ref = -INFINITY;  // log2-domain exponent reference (the O accumulator's units)
-    float lsum = 0.f;         // (bf16 P variant only)
-    uint8_t* prow = sP + (2 * t) * P_BYTES + r * 128;
-    const uint32_t sw = (uint32_t)(r & 7);
-
+    int G = 0;
 #pragma unroll 1
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[2 * t + (j & 1)], (j >> 1) & 1);
-      tc_fence_after();
-      float s[BKV];
-      tmem_ld32(lane_base + S_COL(t, j & 1), *reinterpret_cast<float(*)[32]>(&s[0]));
-      tmem_ld32(lane_base + S_COL(t, j & 1) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-      tmem_ld_wait();
-#if SF_ATTN_SFREE
-      tc_fence_before();
-      mbar_arrive(&s_free[2 * t + (j & 1)]);  // the MMA may overwrite this S buffer now
-#endif
-      float mx[8];
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      float m_ref = -INFINITY;  // log2-domain exponent reference (the O accumulator's units)
+#pragma unroll 1
+      for (int j = 0; j < nkv; ++j, ++G) {
+        const int b = j & 1;
+        mbar_wait(&s_full[2 * t + b], (G >> 1) & 1);
+        if (lane == 0 && quarter == 0) ATR(2 * t, G);
+        tc_fence_after();
+        float s[BKV];
+        tmem_ld32(lane_base + S_COL(t, b), *reinterpret_cast<float(*)[32]>(&s[0]));
+        tmem_ld32(lane_base + S_COL(t, b) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+        tmem_ld_wait();
+        float mx[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx[i] = s[i];
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(s[i], s[i + 8]);
 #pragma unroll
-      for (int i = 8; i < BKV; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
-      const float m_tile = L2E * fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      if (j == 0) {
-        m_ref = m_tile;
-      } else {
-        const bool grow = m_tile > m_ref + RESCALE_LOG2;
-        if (__any_sync(0xffffffffu, grow)) {
-          // the PV of tile j-1 must land in O before O is rescaled
-          mbar_wait(&o_full[2 * t + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-          tc_fence_after();
-          const float a = grow ? ex2(m_ref - m_tile) : 1.0f;
-          if (grow) m_ref = m_tile;
+        for (int i = 16; i < BKV; i += 16)
 #pragma unroll
-          for (int h = 0; h < 3; ++h) {  // O and its l column (+16 padding columns)
-            float ov[32];
-            tmem_ld32(o_addr + 32 * h, ov);
-            tmem_ld_wait();
+          for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], fmaxf(s[i + q], s[i + 8 + q]));
+        const float m_tile = L2E * fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if (j == 0) {
+          m_ref = m_tile;
+        } else {
+          const bool grow = m_tile > m_ref + RESCALE_LOG2;
+          if (__any_sync(0xffffffffu, grow)) {
+            // PV_t(j-1) must have landed in O before O is rescaled
+            mbar_wait(&o_full[2 * t + (b ^ 1)], ((G - 1) >> 1) & 1);
+            tc_fence_after();
+            const float a = grow ? ex2(m_ref - m_tile) : 1.0f;
+            if (grow) m_ref = m_tile;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] *= a;
-            tmem_st32(o_addr + 32 * h, ov);
+            for (int h = 0; h < 5; ++h) {  // O (64) and its l column (+15 zero columns)
+              float ov[16];
+              tmem_ld16(o_addr + 16 * h, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ov[i] *= a;
+              tmem_st16(o_addr + 16 * h, ov);
+            }
+            tmem_st_wait();
           }
-          tmem_st_wait();
         }
-      }
-      // P buffer j%2 was last read by the PV of tile j-2
-      if (j >= 2) mbar_wait(&o_full[2 * t + (j & 1)], ((j - 2) >> 1) & 1);
-      uint8_t* pbuf = prow + (j & 1) * P_BYTES;
+        const float2 l2e2 = make_float2(L2E, L2E), negm = make_float2(-m_ref, -m_ref);
 #pragma unroll
-      for (int c = 0; c < BKV / 8; ++c) {  // 8 chunks of 8 columns = one 16-byte P chunk each
-        uint32_t pk[4];
+        for (int c = 0; c < BKV / 32; ++c) {
+          uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          // two exponentials per MUFU op: x in f16 (|x| <= 8 + range of s), P in f16
-#if SF_ATTN_F16PV
-          pk[i] = ex2_f16x2(fmaf(s[8 * c + 2 * i], L2E, -m_ref), fmaf(s[8 * c + 2 * i + 1], L2E, -m_ref));
-#else
-          const float p0 = ex2(fmaf(s[8 * c + 2 * i], L2E, -m_ref)), p1 = ex2(fmaf(s[8 * c + 2 * i + 1], L2E, -m_ref));
-          lsum += p0 + p1;
-          pk[i] = pack_bf16(p0, p1);
-#endif
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), l2e2, negm);
+            float2 p;
+            if (i < SF_ATTN_EMU_PAIRS) {
+              p = exp2_poly2(x);
+            } else {
+              p.x = ex2(x.x);
+              p.y = ex2(x.y);
+            }
+            pk[i] = pack_f16(p.x, p.y);
+          }
+          tmem_st16u(lane_base + P_COL(t, b) + 16 * c, pk);
         }
-        *reinterpret_cast<uint4*>(pbuf + (((uint32_t)c ^ sw) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * t + b]);
+        if (lane == 0 && quarter == 0) ATR(2 * t + 1, G);
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&p_full[2 * t + (j & 1)]);
-    }
-    // epilogue: O / l -> bf16 -> out[row*T + q, head*64 ...]  (PVs complete in issue order)
-    mbar_wait(&o_full[2 * t + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
-    tc_fence_after();
-    float lv[32];
-    tmem_ld32(o_addr + 64, lv);  // column 64 = sum_k P[r, k] (ones-row of V^T), exactly the P the MMA saw
-    tmem_ld_wait();
-#if SF_ATTN_F16PV
-    const float inv = 1.0f / lv[0];
-#else
-    const float inv = 1.0f / (lv[0] * 0.0f + lsum);
-#endif
-    const int row = bh / heads, head = bh % heads;
-    __nv_bfloat16* dst = out + ((int64_t)row * T + q0 + t * BQ + r) * (heads * HD) + head * HD;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float ov[32];
-      tmem_ld32(o_addr + 32 * h, ov);
+      // epilogue: O / l -> bf16 -> out[row*T + q, head*64 ...]
+      mbar_wait(&o_full[2 * t + 1], ((G - 1) >> 1) & 1);  // last PV (odd buffer); earlier PVs completed before it
+      tc_fence_after();
+      float ov[64], lv[16];
+      tmem_ld32(o_addr, *reinterpret_cast<float(*)[32]>(&ov[0]));
+      tmem_ld32(o_addr + 32, *reinterpret_cast<float(*)[32]>(&ov[32]));
+      tmem_ld16(o_addr + 64, lv);
       tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&o_free[t]);
+      const float inv = 1.0f / lv[0];  // column 64 = sum_k P[r, k], exactly the P the MMA saw
+      const int bh = item / qpairs, q0 = (item % qpairs) * 2 * BQ;
+      const int row = bh / heads, head = bh % heads;
+      __nv_bfloat16* dst = out + ((int64_t)row * T + q0 + t * BQ + r) * (heads * HD) + head * HD;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        reinterpret_cast<uint4*>(dst + 32 * h)[i] =
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<uint4*>(dst)[i] =
             make_uint4(pack_bf16(ov[8 * i] * inv, ov[8 * i + 1] * inv), pack_bf16(ov[8 * i + 2] * inv, ov[8 * i + 3] * inv),
                        pack_bf16(ov[8 * i + 4] * inv, ov[8 * i + 5] * inv), pack_bf16(ov[8 * i + 6] * inv, ov[8 * i + 7] * inv));
     }
@@ -320,6 +401,17 @@ int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, in
   return SF_OK;
 }
 
+static int attn_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 int prepare_attn_kernel() {
   static bool attr = false;
   if (!attr) {
@@ -333,12 +425,19 @@ int prepare_attn_kernel() {
 
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st) {
   if (prepare_attn_kernel() != SF_OK) return SF_ERR_CUDA;
-  dim3 grid(T / (2 * attn::BQ), (unsigned)(rows * heads));
-  attn_fwd_tcgen05<<<grid, attn::THREADS, attn::SMEM, st>>>(m.q, m.k, m.v, out, T, heads);
+  const int64_t items = rows * heads * (T / (2 * attn::BQ));
+  const int grid = (int)(items < attn_sm_count() ? items : attn_sm_count());
+  attn_fwd_tcgen05<<<grid, attn::THREADS, attn::SMEM, st>>>(m.q, m.k, m.v, out, T, heads, (int)items);
   return cuda_status();
 }
 
 }  // namespace sf
+
+#if SF_ATTN_TRACE
+extern "C" int sf_attn_trace_read(long long* dst) {
+  return cudaMemcpyFromSymbol(dst, sf::g_attn_trace, sizeof(long long) * 8 * 64) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int sf_attention(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads,
                             int32_t T, void* stream) {
