@@ -32,12 +32,6 @@
 #include "sf_internal.h"
 #include "sf_ptx.cuh"
 
-#ifndef SF_ATTN_SAFE_S
-#define SF_ATTN_SAFE_S 0  // diagnostics: wait for PV_t(j) before S_t(j+2) reuses its buffer
-#endif
-#ifndef SF_ATTN_DESYNC
-#define SF_ATTN_DESYNC 0
-#endif
 #ifndef SF_ATTN_TRACE
 #define SF_ATTN_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_attn_trace_read)
 #endif
@@ -48,7 +42,7 @@
 namespace sf {
 
 #if SF_ATTN_TRACE
-__device__ long long g_attn_trace[8 * 64];
+__device__ long long g_attn_trace[16 * 64];
 #define ATR(role, idx)                                                               \
   do {                                                                               \
     if (blockIdx.x == 0 && (idx) < 64) g_attn_trace[(role) * 64 + (idx)] = clock64(); \
@@ -227,68 +221,67 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       }
     }
   } else if (warp == 9 || warp == 10) {
-    if (lane == 0) {
-      // ---------------- MMA issuer, one per query tile (the two progress independently)
-      const int t = warp - 9;
-      constexpr uint32_t idesc_s = idesc_bf16_f32(128, BKV);
-      constexpr uint32_t idesc_pv = (1u << 4) | ((uint32_t)V_ROWS >> 3 << 17) | ((128u >> 4) << 24);  // f16 A/B
-      auto issue_s = [&](int qb, int s, int b) {
-        const uint32_t q_addr = smem_u32(sQ + qb * Q_BYTES + t * Q_TILE);
-        const uint32_t k_addr = smem_u32(sKV + s * STAGE);
+    // ---------------- MMA issuer, one warp per query tile (the two progress independently).
+    // The whole warp runs the loop so every operand is warp-uniform (uniform
+    // registers, no per-MMA R2UR waterfall); one elected lane issues.
+    const int t = warp - 9;
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, BKV);
+    constexpr uint32_t idesc_pv = (1u << 4) | ((uint32_t)V_ROWS >> 3 << 17) | ((128u >> 4) << 24);  // f16 A/B
+    const uint64_t q_desc0 = sw128_kmajor_desc(smem_u32(sQ + t * Q_TILE));
+    const uint64_t kv_desc0 = sw128_kmajor_desc(smem_u32(sKV));
+    // descriptor address field is addr >> 4: +32 B per K step = +2, +STAGE per stage
+    auto issue_s = [&](int qb, int s, int b) {
+      const uint64_t qd = q_desc0 + (uint64_t)((qb * Q_BYTES) >> 4);
+      const uint64_t kd = kv_desc0 + (uint64_t)((s * STAGE) >> 4);
+      if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          mma_bf16_ss(tmem + S_COL(t, b), sw128_kmajor_desc(q_addr + k * 32), sw128_kmajor_desc(k_addr + k * 32),
-                      idesc_s, k != 0);
+        for (int k = 0; k < HD / 16; ++k) mma_bf16_ss(tmem + S_COL(t, b), qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
         mma_commit(&s_full[2 * t + b]);
-      };
-      auto issue_pv = [&](int s, int b, bool acc) {
-        const uint32_t v_addr = smem_u32(sKV + s * STAGE + K_BYTES);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int s, int b, bool acc) {
+      const uint64_t vd = kv_desc0 + (uint64_t)((s * STAGE + K_BYTES) >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, sw128_kmajor_desc(v_addr + k * 32), idesc_pv,
-                     acc || k != 0);
+          mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, vd + 2 * k, idesc_pv, acc || k != 0);
         mma_commit(&o_full[2 * t + b]);
-      };
-      int kv = 0, local = 0;
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
-        const int qb = local & 1;
-        mbar_wait(&q_full[qb], (local >> 1) & 1);
-#if SF_ATTN_SAFE_S
-        if (kv > 0) mbar_wait(&o_full[2 * t + 1], ((kv - 1) >> 1) & 1);
-#endif
-#if SF_ATTN_DESYNC
-        // start tile B half a softmax behind tile A so their latency phases interleave
-        if (t == 1 && kv == 0) mbar_wait(&s_full[0], 0);
-#endif
-        for (int j = 0; j < 2; ++j) {
-          const int G = kv + j;
-          mbar_wait(&kv_full[G % KV_STAGES], (G / KV_STAGES) & 1);
-          tc_fence_after();
-          issue_s(qb, G % KV_STAGES, j);
-        }
+        mma_commit(&kv_empty[s]);
+      }
+      __syncwarp();
+    };
+    int kv = 0, local = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
+      const int qb = local & 1;
+      mbar_wait(&q_full[qb], (local >> 1) & 1);
+      for (int j = 0; j < 2; ++j) {
+        const int G = kv + j;
+        mbar_wait(&kv_full[G % KV_STAGES], (G / KV_STAGES) & 1);
+        tc_fence_after();
+        issue_s(qb, G % KV_STAGES, j);
+      }
 #pragma unroll 1
-        for (int j = 0; j < nkv; ++j) {
-          const int G = kv + j, b = j & 1;
-          mbar_wait(&p_full[2 * t + b], (G >> 1) & 1);          // P_t(j) in TMEM, O_t rescaled
-          ATR(4 + 2 * t, G);
-          if (j == 0) mbar_wait(&o_free[t], (local & 1) ^ 1);  // previous item's O read out
+      for (int j = 0; j < nkv; ++j) {
+        const int G = kv + j, b = j & 1;
+        mbar_wait(&p_full[2 * t + b], (G >> 1) & 1);          // P_t(j) in TMEM, O_t rescaled
+        if (lane == 0) ATR(4 + 2 * t, G);
+        if (j == 0) mbar_wait(&o_free[t], (local & 1) ^ 1);  // previous item's O read out
+        tc_fence_after();
+        issue_pv(G % KV_STAGES, b, j != 0);
+        if (j + 2 < nkv) {
+          // S_t(j+2) reuses buffer b: issued after PV_t(j), which reads P_t(j) from it
+          mbar_wait(&kv_full[(G + 2) % KV_STAGES], ((G + 2) / KV_STAGES) & 1);
           tc_fence_after();
-          issue_pv(G % KV_STAGES, b, j != 0);
-          mma_commit(&kv_empty[G % KV_STAGES]);
-          if (j + 2 < nkv) {
-            // S_t(j+2) reuses buffer b: issued after PV_t(j), which reads P_t(j) from it
-            mbar_wait(&kv_full[(G + 2) % KV_STAGES], ((G + 2) / KV_STAGES) & 1);
-#if SF_ATTN_SAFE_S
-            mbar_wait(&o_full[2 * t + b], (G >> 1) & 1);
-#endif
-            tc_fence_after();
-            ATR(5 + 2 * t, G + 2);
-            issue_s(qb, (G + 2) % KV_STAGES, b);
-            if (j + 3 == nkv) mma_commit(&q_empty[qb]);  // last S of this tile on this Q
+          if (lane == 0) ATR(5 + 2 * t, G + 2);
+          issue_s(qb, (G + 2) % KV_STAGES, b);
+          if (j + 3 == nkv) {
+            if (elect_one()) mma_commit(&q_empty[qb]);  // last S of this tile on this Q
+            __syncwarp();
           }
         }
-        kv += nkv;
       }
+      kv += nkv;
     }
   } else {
     // ---------------- softmax warpgroups: warps 0-3 -> tile A, 4-7 -> tile B
@@ -312,6 +305,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         tmem_ld32(lane_base + S_COL(t, b), *reinterpret_cast<float(*)[32]>(&s[0]));
         tmem_ld32(lane_base + S_COL(t, b) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
         tmem_ld_wait();
+        if (lane == 0 && quarter == 0) ATR(8 + 4 * t, G);  // S in registers
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = fmaxf(s[i], s[i + 8]);
@@ -343,6 +337,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
             tmem_st_wait();
           }
         }
+        if (lane == 0 && quarter == 0) ATR(9 + 4 * t, G);  // max + rescale check done
         const float2 l2e2 = make_float2(L2E, L2E), negm = make_float2(-m_ref, -m_ref);
 #pragma unroll
         for (int c = 0; c < BKV / 32; ++c) {
@@ -361,7 +356,9 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
           }
           tmem_st16u(lane_base + P_COL(t, b) + 16 * c, pk);
         }
+        if (lane == 0 && quarter == 0) ATR(10 + 4 * t, G);  // P computed, stores issued
         tmem_st_wait();
+        if (lane == 0 && quarter == 0) ATR(11 + 4 * t, G);  // stores complete
         tc_fence_before();
         mbar_arrive(&p_full[2 * t + b]);
         if (lane == 0 && quarter == 0) ATR(2 * t + 1, G);
@@ -435,7 +432,7 @@ int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, 
 
 #if SF_ATTN_TRACE
 extern "C" int sf_attn_trace_read(long long* dst) {
-  return cudaMemcpyFromSymbol(dst, sf::g_attn_trace, sizeof(long long) * 8 * 64) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(dst, sf::g_attn_trace, sizeof(long long) * 16 * 64) == cudaSuccess ? 0 : -1;
 }
 #endif
 
