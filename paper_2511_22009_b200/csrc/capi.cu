@@ -18,7 +18,7 @@ int sf_device_sm_count(void) {
 int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
                  int32_t epi, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % 128) return SF_ERR_PARAMETER;
-  const int no_store = (epi & 0x100) ? 1 : 0;  // diagnostics flag (not part of the documented ABI values)
+  const int no_store = (epi & 0x200) ? 2 : (epi & 0x100) ? 1 : 0;  // diagnostics flags (not part of the documented ABI values)
   epi &= 0xff;
   if (epi < EPI_F32 || epi > EPI_GELU) return SF_ERR_PARAMETER;
   const int bn = (N % 256 == 0) ? 256 : 128;
@@ -51,13 +51,20 @@ int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* 
   return launch_gemm(EPI_QKV, 192, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
+// Diagnostics only (not in the header): 1 = skip epilogue stores, 2 = main loop only.
+static int g_diag_res_ln = 0;
+int sf_diag_res_ln(int mode) {
+  g_diag_res_ln = mode;
+  return 0;
+}
+
 int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, void* xmod, const float* gate,
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream) {
   if (N != 384 || K % 64 || M < 1 || M % tokens_per_slot || tokens_per_slot % 128) return SF_ERR_PARAMETER;
   GemmMaps maps;
   if (make_operand_maps(&maps, A, M, K, W, N, 384) != SF_OK) return SF_ERR_CUDA;
-  if (make_out_map(&maps.d[0], xres, M, N) != SF_OK || make_out_map(&maps.d[1], xmod, M, N) != SF_OK)
+  if (make_out_map32(&maps.d[0], xres, M, N) != SF_OK || make_out_map32(&maps.d[1], xmod, M, N) != SF_OK)
     return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
@@ -69,6 +76,7 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
   ep.ln_eps = ln_eps;
   ep.tokens_per_slot = tokens_per_slot;
   ep.M = (int)M;
+  ep.no_store = g_diag_res_ln;
   return launch_gemm(EPI_RES_LN, 384, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 

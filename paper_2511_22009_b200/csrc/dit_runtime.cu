@@ -545,13 +545,13 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, 192);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
     rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
-    rc |= make_out_map(&h->g_proj[l].d[0], h->xres, M, H);
-    rc |= make_out_map(&h->g_proj[l].d[1], h->xmod, M, H);
+    rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);
+    rc |= make_out_map32(&h->g_proj[l].d[1], h->xmod, M, H);
     rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
     rc |= make_out_map(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);
     rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 384);
-    rc |= make_out_map(&h->g_fc2[l].d[0], h->xres, M, H);
-    rc |= make_out_map(&h->g_fc2[l].d[1], h->xmod, M, H);
+    rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
+    rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
   if (rc != SF_OK) {

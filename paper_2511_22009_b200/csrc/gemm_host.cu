@@ -1,3 +1,4 @@
+#include <cstdio>
 // Host side of the tcgen05 GEMM: TMA descriptor encoding + launch dispatch.
 #include <cudaTypedefs.h>
 
@@ -57,6 +58,11 @@ int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols) {
   return make_tmap_bf16_2d(m, D, cols, rows, cols, 64, 32, 128);
 }
 
+// Output map for the RES_LN epilogue: 32-row x 32-column chunks (64B swizzle).
+int make_out_map32(CUtensorMap* m, const void* D, int64_t rows, int64_t cols) {
+  return make_tmap_bf16_2d(m, D, cols, rows, cols, 32, 32, 64);
+}
+
 // QKV outputs: Q, K [rows*H*T, 64] and V^T [rows*H*64, T] (32-token x 64-dim chunks, 64B swizzle).
 int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T) {
   const int64_t bh = rows * heads;
@@ -68,7 +74,7 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
 
 template <int BN, int KIND>
 constexpr int epi_warps() {
-  return KIND == EPI_QKV ? 4 : 8;
+  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;
 }
 
 template <int BN, int KIND>
@@ -76,9 +82,13 @@ static int set_attr() {
   static bool done = false;
   if (!done) {
     constexpr int W = epi_warps<BN, KIND>();
-    if (cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<BN, W>::SMEM_BYTES) != cudaSuccess)
+    const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, W>::SMEM_BYTES);
+    if (err != cudaSuccess) {
+      fprintf(stderr, "streamflow: gemm<%d,%d> smem attribute (%d B) failed: %s\n", BN, KIND, GemmCfg<BN, W>::SMEM_BYTES,
+              cudaGetErrorString(err));
       return SF_ERR_CUDA;
+    }
     done = true;
   }
   return SF_OK;
@@ -120,7 +130,13 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
   EpiParams e = ep;
   e.M = M;
   gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(maps, N, K, e);
-  return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    fprintf(stderr, "streamflow: gemm<%d,%d> launch failed: %s (smem %d, threads %d)\n", BN, KIND,
+            cudaGetErrorString(err), C::SMEM_BYTES, C::THREADS);
+    return SF_ERR_CUDA;
+  }
+  return SF_OK;
 }
 
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,

@@ -72,17 +72,23 @@ struct GemmCfg {
   static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;  // column offset between accumulator stages
   static constexpr int TMEM_COLS = ACC_STAGES == 2 ? (BN <= 128 ? 256 : 512) : (BN <= 256 ? 256 : 512);
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-  static constexpr int RED_BYTES = 2 * 8 * 32 * 4;      // LN partial sums of paired epilogue warps
-  static constexpr int VEC_BYTES = 2 * 4 * BN * 4;      // per-tile column vectors, double-buffered
-  static constexpr int OUT_BYTES = EPI_WARPS * 2 * 4096;  // per-warp output staging, double-buffered
-  static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES;
+  static constexpr int RED_BYTES = 2 * EPI_WARPS * 32 * 4;  // LN partial sums of the warps sharing a row
+  static constexpr int VEC_BYTES = 2 * 4 * BN * 4;          // per-tile column vectors, double-buffered
+  // per-warp output staging, double-buffered: 32 rows x 128 B (SW128), or 32 x 64 B (SW64) with 12 warps
+  // (RES_LN: a 3-deep ring per warp; residual chunks are TMA-loaded into it and
+  // overwritten in place by the updated residual before its TMA store)
+  static constexpr int OUT_BUF = EPI_WARPS == 12 ? 2048 : 4096;
+  static constexpr int OUT_NBUF = EPI_WARPS == 12 ? 3 : 2;
+  static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
+  static constexpr int RBAR_BYTES = EPI_WARPS * 3 * 8;  // residual-chunk barriers (RES_LN ring)
+  static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES + RBAR_BYTES;
   static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int SMEM_BYTES = FIXED + STAGES * STAGE_BYTES;
   static_assert(STAGES >= 3, "pipeline too shallow");
   static_assert(MMA_N % 16 == 0 && MMA_N <= 256, "bad MMA N");
   static_assert(B_BOX <= 256, "bad box");
-  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
+  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8 || EPI_WARPS == 12, "epilogue warps");
 };
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -105,18 +111,23 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t smem_addr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
-// Per-warp output staging: a 32-row x 128-byte tile in the TMA 128B-swizzle
-// layout.  Lane = row; 16-byte chunk c of the row lives at chunk c ^ (row & 7).
-struct OutStage {
-  uint8_t* base;     // this warp's 2 x 4 KB
+// Per-warp output staging: a 32-row tile in the TMA swizzle layout, 128-byte
+// rows (SW128: 16-byte chunk c of row r at c ^ (r & 7)) or 64-byte rows (SW64:
+// chunk c at c ^ ((r >> 1) & 3)).  Lane = row.
+template <int BUF>
+struct OutStageT {
+  uint8_t* base;     // this warp's 2 x BUF bytes
   uint32_t count;    // chunks issued so far by this warp (buffer = count & 1)
   __device__ __forceinline__ uint8_t* acquire(uint32_t lane) {
     if (count >= 2 && lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago left this buffer
     __syncwarp();
-    return base + (count & 1) * 4096;
+    return base + (count & 1) * BUF;
   }
   __device__ __forceinline__ static void put16(uint8_t* buf, uint32_t row, uint32_t chunk, uint4 v) {
-    *reinterpret_cast<uint4*>(buf + row * 128 + ((chunk ^ (row & 7)) * 16)) = v;
+    if constexpr (BUF == 4096)
+      *reinterpret_cast<uint4*>(buf + row * 128 + ((chunk ^ (row & 7)) * 16)) = v;
+    else
+      *reinterpret_cast<uint4*>(buf + row * 64 + ((chunk ^ ((row >> 1) & 3)) * 16)) = v;
   }
   __device__ __forceinline__ void release(uint32_t lane, const CUtensorMap* map, uint8_t* buf, int c0, int c1,
                                           bool store) {
@@ -135,8 +146,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ GemmMaps maps, int N, int K, EpiParams ep) {
   using C = GemmCfg<BN, EPI_WARPS>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sOut = smem;                             // [EPI_WARPS][2][4096]   (1024-aligned)
+  // 1024-align by offsetting into the shared array (keeps the pointer in the shared window: LDS/STS, not generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sOut = smem;                             // [EPI_WARPS][OUT_NBUF][OUT_BUF]   (1024-aligned)
   uint8_t* sA = sOut + C::OUT_BYTES;                // [STAGES][A_BYTES]
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;        // [STAGES][B_BYTES]
   float* red = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);  // [2][8 warps][32]
@@ -147,6 +159,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + C::ACC_STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::ACC_STAGES);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [EPI_WARPS][3]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -166,6 +179,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS * 32);
     }
+    if constexpr (KIND == EPI_RES_LN)
+      for (int i = 0; i < EPI_WARPS * 3; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
@@ -193,31 +208,36 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(128, C::MMA_N);
-      uint32_t it = 0, local = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
-        const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
+    // ---------------- MMA issuer: the whole warp runs the loop so descriptors
+    // stay warp-uniform (uniform registers, no per-MMA R2UR waterfall); one
+    // elected lane issues.  Descriptor address field = addr >> 4.
+    constexpr uint32_t idesc = idesc_bf16_f32(128, C::MMA_N);
+    const uint64_t a_desc0 = kmajor_desc<C::SWZ>(smem_u32(sA));
+    const uint64_t b_desc0 = kmajor_desc<C::SWZ>(smem_u32(sB));
+    uint32_t it = 0, local = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
+      const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + s * C::B_BYTES);
+        const uint64_t ad = a_desc0 + (uint64_t)((s * C::A_BYTES) >> 4);
+        const uint64_t bd = b_desc0 + (uint64_t)((s * C::B_BYTES) >> 4);
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k) {
 #pragma unroll
             for (int h = 0; h < C::N_SPLIT; ++h)
-              mma_bf16_ss(d + h * C::MMA_N, kmajor_desc<C::SWZ>(a_addr + k * 32),
-                          kmajor_desc<C::SWZ>(b_addr + h * C::MMA_N * C::SWZ + k * 32), idesc, (kb | k) != 0);
+              mma_bf16_ss(d + h * C::MMA_N, ad + 2 * k, bd + (uint64_t)((h * C::MMA_N * C::SWZ) >> 4) + 2 * k, idesc,
+                          (kb | k) != 0);
           }
           mma_commit(&empty[s]);
+          if (kb + 1 == num_kb) mma_commit(&tfull[acc]);
         }
-        mma_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else {
@@ -225,10 +245,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     const uint32_t e = warp - 2;
     const uint32_t quarter = warp & 3;
     constexpr int EPI_THREADS = EPI_WARPS * 32;
-    constexpr int COLS = EPI_WARPS == 8 ? BN / 2 : BN;
-    const int c_lo = EPI_WARPS == 8 ? (int)(e / 4) * COLS : 0;
+    constexpr int COLS = BN / (EPI_WARPS / 4);  // columns per thread (warps sharing a lane quarter split them)
+    const int c_lo = (int)(e / 4) * COLS;
     const int et = threadIdx.x - 64;
-    OutStage out{sOut + e * 8192, 0};
+    using OutStage = OutStageT<C::OUT_BUF>;
+    OutStage out{sOut + e * C::OUT_NBUF * C::OUT_BUF, 0};
+    uint32_t ring = 0, rpar = 0;  // RES_LN: ring uses so far, per-buffer load parity bits
     const bool do_store = !ep.no_store;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
@@ -252,18 +274,31 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           vb[3 * BN + c] = ep.scale[o];
         }
       }
-      constexpr int PF = 2;  // RES_LN: residual chunks (32 columns) in flight
-      uint4 old[KIND == EPI_RES_LN ? PF : 1][4];
-      const uint4* old_src = reinterpret_cast<const uint4*>(ep.xres + (int64_t)row * N + n0 + c_lo);
+      // RES_LN: residual chunks (32 rows x 32 columns) are TMA-loaded into this
+      // warp's staging ring; the first two are issued before the accumulator wait
+      // so their latency hides under the main loop.
+      uint8_t* const rbuf0 = sOut + e * C::OUT_NBUF * C::OUT_BUF;
+      auto res_load = [&](uint32_t use, int q) {  // lane 0: residual chunk q into the buffer of ring use `use`
+        const uint32_t b = use % 3;
+        mbar_expect_tx(&rbar[e * 3 + b], C::OUT_BUF);
+        tma_load_2d(rbuf0 + b * C::OUT_BUF, &maps.d[0], &rbar[e * 3 + b], n0 + c_lo + 32 * q, r0);
+      };
       if constexpr (KIND == EPI_RES_LN) {
-#pragma unroll
-        for (int q = 0; q < PF; ++q)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) old[q][i] = valid ? old_src[4 * q + i] : make_uint4(0, 0, 0, 0);
+        if (lane == 0) {
+          bulk_wait_read<1>();  // the previous users of these two buffers (stores) have read them
+          res_load(ring, 0);
+          res_load(ring + 1, 1);
+        }
+        __syncwarp();
       }
       named_bar_sync(5, EPI_THREADS);  // vectors staged
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (ep.no_store == 2) {  // diagnostics: main loop only
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       const float* vbias = vb + c_lo;
 
       if constexpr (KIND == EPI_F32) {
@@ -364,82 +399,94 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
             out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_RES_LN) {
-        static_assert(KIND != EPI_RES_LN || (EPI_WARPS == 8 && COLS % 64 == 0), "RES_LN pairs two warps per row");
+        // 12 epilogue warps: the 3 warps of a lane quarter split each 384-column
+        // row into 128-column thirds (4 chunks of 32); 32-column chunks are
+        // staged in 64B-swizzled smem and stored by TMA (box 32 x 32).
+        static_assert(KIND != EPI_RES_LN || (EPI_WARPS == 12 && COLS % 32 == 0), "RES_LN layout");
         const float* vgate = vb + BN + c_lo;
         const float* vshift = vb + 2 * BN + c_lo;
         const float* vscale = vb + 3 * BN + c_lo;
         const uint32_t tcol = taddr + c_lo;
         const bool st_ok = do_store && r0 < ep.M;
-        // pass 1: x_new = x + gate*(acc + bias) -> bf16 residual (TMA store) and its
-        // rounded fp32 value back into TMEM; partial row sum over this half
+        // pass 1: x_new = x + gate*(acc + bias) -> bf16 residual (TMA store), kept in
+        // registers as bf16 pairs (LayerNorm sees the stored, rounded residual);
+        // partial row sum.  The accumulator is released right after its last TMEM
+        // read, so the next tile's main loop overlaps the LayerNorm passes.
+        constexpr int NQ = COLS / 32;
+        uint32_t xr[NQ][16];
         float sum = 0.f;
-        uint8_t* buf = nullptr;
 #pragma unroll
-        for (int q = 0; q < COLS / 32; ++q) {
-          if ((q & 1) == 0) buf = out.acquire(lane);
-          float v[32];
-          tmem_ld32(tcol + 32 * q, v);
-          tmem_ld_wait();
-          uint4 cur[4];
+        for (int q = 0; q < NQ; ++q) {
+          const uint32_t b = (ring + q) % 3;
+          uint8_t* buf = rbuf0 + b * C::OUT_BUF;
+          mbar_wait(&rbar[e * 3 + b], (rpar >> b) & 1);
+          rpar ^= 1u << b;
+          uint4 oldv[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) cur[i] = old[q % PF][i];
-          if (q + PF < COLS / 32) {
+          for (int i = 0; i < 4; ++i)
+            oldv[i] = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((i ^ ((lane >> 1) & 3)) * 16));
+          const uint32_t* ow = reinterpret_cast<const uint32_t*>(oldv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) old[q % PF][i] = valid ? old_src[4 * (q + PF) + i] : make_uint4(0, 0, 0, 0);
-          }
-          uint32_t packed[16];
+          for (int hh = 0; hh < 2; ++hh) {
+            const int u = 2 * q + hh;  // 16-column sub-chunk
+            float v[16];
+            tmem_ld16(tcol + 16 * u, v);
+            tmem_ld_wait();
+            if (u + 1 == 2 * NQ) {  // last TMEM read: the next tile's main loop may start
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 bb = reinterpret_cast<const float4*>(vbias + 32 * q)[i];
-            const float4 g = reinterpret_cast<const float4*>(vgate + 32 * q)[i];
-            const uint32_t* ow = reinterpret_cast<const uint32_t*>(cur);
-            const float2 o0 = unpack_bf16(ow[2 * i]), o1 = unpack_bf16(ow[2 * i + 1]);
-            packed[2 * i] = pack_bf16(o0.x + g.x * (v[4 * i] + bb.x), o0.y + g.y * (v[4 * i + 1] + bb.y));
-            packed[2 * i + 1] = pack_bf16(o1.x + g.z * (v[4 * i + 2] + bb.z), o1.y + g.w * (v[4 * i + 3] + bb.w));
-            const float2 r0v = unpack_bf16(packed[2 * i]), r1v = unpack_bf16(packed[2 * i + 1]);
-            v[4 * i] = r0v.x;  // LayerNorm sees the stored (rounded) residual
-            v[4 * i + 1] = r0v.y;
-            v[4 * i + 2] = r1v.x;
-            v[4 * i + 3] = r1v.y;
-            sum += (r0v.x + r0v.y) + (r1v.x + r1v.y);
+            for (int i = 0; i < 4; ++i) {
+              const float4 bb = reinterpret_cast<const float4*>(vbias + 16 * u)[i];
+              const float4 g = reinterpret_cast<const float4*>(vgate + 16 * u)[i];
+              const int w = 8 * hh + 2 * i;
+              const float2 o0 = unpack_bf16(ow[w]), o1 = unpack_bf16(ow[w + 1]);
+              xr[q][w] = pack_bf16(o0.x + g.x * (v[4 * i] + bb.x), o0.y + g.y * (v[4 * i + 1] + bb.y));
+              xr[q][w + 1] = pack_bf16(o1.x + g.z * (v[4 * i + 2] + bb.z), o1.y + g.w * (v[4 * i + 3] + bb.w));
+              const float2 r0v = unpack_bf16(xr[q][w]), r1v = unpack_bf16(xr[q][w + 1]);
+              sum += (r0v.x + r0v.y) + (r1v.x + r1v.y);
+            }
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            OutStage::put16(buf, lane, 4 * (q & 1) + i,
-                            make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]));
-          if (q & 1) out.release(lane, &maps.d[0], buf, n0 + c_lo + 32 * (q - 1), r0, st_ok);
-          tmem_st32(tcol + 32 * q, v);
+            OutStage::put16(buf, lane, i, make_uint4(xr[q][4 * i], xr[q][4 * i + 1], xr[q][4 * i + 2], xr[q][4 * i + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (st_ok) tma_store_2d(&maps.d[0], buf, n0 + c_lo + 32 * q, r0);
+            bulk_commit();
+            if (q + 2 < NQ) {
+              bulk_wait_read<1>();  // the store that last used the next buffer has read it
+              res_load(ring + q + 2, q + 2);
+            }
+          }
+          __syncwarp();
         }
-        tmem_st_wait();
-        // the two warps of this lane quarter hold the two halves of each row
+        // the 3 warps of this lane quarter hold the 3 thirds of each row
+        const uint32_t eq = e & 3;
         red[e * 32 + lane] = sum;
-        named_bar_sync(1 + quarter, 64);
-        const float mean = (sum + red[(e ^ 4) * 32 + lane]) * (1.0f / N);
+        named_bar_sync(1 + quarter, 96);
+        const float mean = (red[eq * 32 + lane] + red[(eq + 4) * 32 + lane] + red[(eq + 8) * 32 + lane]) * (1.0f / N);
         float var = 0.f;
-#pragma unroll 1
-        for (int q = 0; q < COLS / 32; ++q) {
-          float v[32];
-          tmem_ld32(tcol + 32 * q, v);
-          tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float dlt = v[i] - mean;
-            var += dlt * dlt;
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 xv = unpack_bf16(xr[q][i]);
+            const float d0 = xv.x - mean, d1 = xv.y - mean;
+            var += d0 * d0 + d1 * d1;
           }
-        }
-        red[256 + e * 32 + lane] = var;
-        named_bar_sync(1 + quarter, 64);
-        const float rstd = rsqrtf((var + red[256 + (e ^ 4) * 32 + lane]) * (1.0f / N) + ep.ln_eps);
-#pragma unroll 1
-        for (int q = 0; q < COLS / 32; ++q) {
-          if ((q & 1) == 0) buf = out.acquire(lane);
-          float v[32];
-          tmem_ld32(tcol + 32 * q, v);
-          tmem_ld_wait();
-          if (q + 1 == COLS / 32) {  // last TMEM read of this tile: hand the accumulator back early
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
-          }
+        float* red2 = red + EPI_WARPS * 32;
+        red2[e * 32 + lane] = var;
+        named_bar_sync(1 + quarter, 96);
+        const float var_all = red2[eq * 32 + lane] + red2[(eq + 4) * 32 + lane] + red2[(eq + 8) * 32 + lane];
+        const float rstd = rsqrtf(var_all * (1.0f / N) + ep.ln_eps);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          uint8_t* buf = rbuf0 + ((ring + NQ + q) % 3) * C::OUT_BUF;
+          if (lane == 0) bulk_wait_read<2>();  // the store 3 uses ago left this buffer
+          __syncwarp();
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             float o[8];
@@ -447,16 +494,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
             for (int k = 0; k < 2; ++k) {
               const float4 sh = reinterpret_cast<const float4*>(vshift + 32 * q)[2 * i + k];
               const float4 sc = reinterpret_cast<const float4*>(vscale + 32 * q)[2 * i + k];
-              const float* vv = v + 8 * i + 4 * k;
-              o[4 * k] = (vv[0] - mean) * rstd * (1.0f + sc.x) + sh.x;
-              o[4 * k + 1] = (vv[1] - mean) * rstd * (1.0f + sc.y) + sh.y;
-              o[4 * k + 2] = (vv[2] - mean) * rstd * (1.0f + sc.z) + sh.z;
-              o[4 * k + 3] = (vv[3] - mean) * rstd * (1.0f + sc.w) + sh.w;
+              const float2 xa = unpack_bf16(xr[q][4 * i + 2 * k]), xb = unpack_bf16(xr[q][4 * i + 2 * k + 1]);
+              o[4 * k] = (xa.x - mean) * rstd * (1.0f + sc.x) + sh.x;
+              o[4 * k + 1] = (xa.y - mean) * rstd * (1.0f + sc.y) + sh.y;
+              o[4 * k + 2] = (xb.x - mean) * rstd * (1.0f + sc.z) + sh.z;
+              o[4 * k + 3] = (xb.y - mean) * rstd * (1.0f + sc.w) + sh.w;
             }
-            OutStage::put16(buf, lane, 4 * (q & 1) + i, pack8_bf16(o));
+            OutStage::put16(buf, lane, i, pack8_bf16(o));
           }
-          if (q & 1) out.release(lane, &maps.d[1], buf, n0 + c_lo + 32 * (q - 1), r0, st_ok);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (st_ok) tma_store_2d(&maps.d[1], buf, n0 + c_lo + 32 * q, r0);
+            bulk_commit();
+          }
+          __syncwarp();
         }
+        ring += 2 * NQ;
       }
     }
     if (lane == 0) bulk_wait<0>();  // all output stores of this warp have landed

@@ -15,6 +15,7 @@ int gemm_bk(int bn);
 int gemm_b_box_rows(int bn);
 int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn);
 int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
+int make_out_map32(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
 int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T);
 int prepare_gemm_kernels();
 int prepare_attn_kernel();
