@@ -162,6 +162,11 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
  * out: [rows * T, heads * 64] bf16 (token-major, heads concatenated). */
 int sf_attention(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads, int32_t T,
                  void* stream);
+/* Same with head dim hd in {64, 72} (DiT-S/2, DiT-XL/2): q, k [rows, heads, T, hd]
+ * bf16, vt [rows, heads, hd, T] fp16, out [rows * T, heads * hd] bf16.  For hd 72
+ * the QK^T contraction is zero-padded to 80 on chip (no padding in memory). */
+int sf_attention_hd(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads, int32_t T,
+                    int32_t hd, void* stream);
 
 /* ---- DiT velocity-field runtime (the network behind VelocityModel.forward,
  * models.py:89-136; it has no reference implementation -- SURVEY 8(c)) ----

@@ -53,6 +53,7 @@ SIGNATURES = {
     "sf_gemm_res_ln": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32,
                        C.c_float, _vp],
     "sf_attention": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
+    "sf_attention_hd": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp],
 }
 
 _lib = None

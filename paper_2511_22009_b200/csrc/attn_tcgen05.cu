@@ -56,17 +56,8 @@ __device__ long long g_attn_trace[16 * 64];
 namespace attn {
 constexpr int BQ = 128;  // queries per tile (2 tiles per item)
 constexpr int BKV = 64;  // keys per KV tile
-constexpr int HD = 64;
-constexpr int Q_TILE = BQ * HD * 2;    // 16 KB
-constexpr int Q_BYTES = 2 * Q_TILE;    // both tiles of an item
-constexpr int K_BYTES = BKV * HD * 2;  // 8 KB (64 kv rows x 128 B)
-constexpr int V_ROWS = HD + 16;        // V^T rows 0..63 from TMA; row 64 = ones (-> l), 65..79 = 0
-constexpr int V_BYTES = V_ROWS * 128;  // 80 rows x 128 B (SW128)
-constexpr int V_TMA = HD * 128;        // bytes loaded per stage
-constexpr int STAGE = K_BYTES + V_BYTES;
 constexpr int KV_STAGES = 6;
 constexpr int QBUF = 2;
-constexpr int SMEM = 1024 + QBUF * Q_BYTES + KV_STAGES * STAGE + 256;
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int TMEM_COLS = 512;
 // S_t,b: tile t, buffer b (64 fp32 columns); P_t,b (fp16 pairs) aliases its upper 32 columns
@@ -75,6 +66,35 @@ __host__ __device__ constexpr uint32_t P_COL(int t, int b) { return 64u * (2 * t
 __host__ __device__ constexpr uint32_t O_COL(int t) { return 256u + 128u * t; }
 constexpr int THREADS = 352;
 }  // namespace attn
+
+// Head-dim dependent layout.  Q / K rows are split into a 64-element part
+// (128-byte rows, SW128) and, for HD > 64, a 16-element part (32-byte rows,
+// SW32) holding head-dim elements 64..79 (72..79 zero-filled by TMA out of
+// bounds), so the QK^T MMA runs over K = 80.  V^T tiles hold HD data rows, a
+// ones-row at HD (-> softmax row sum in O column HD) and zero rows up to 80.
+template <int HD>
+struct AttnCfg {
+  static_assert(HD == 64 || HD == 72, "head dim");
+  static constexpr int HI = HD > 64 ? 16 : 0;
+  static constexpr int KSTEPS = (64 + HI) / 16;
+  static constexpr int Q_LO = attn::BQ * 128;
+  static constexpr int Q_TILE = Q_LO + attn::BQ * HI * 2;   // 16 / 20 KB
+  static constexpr int Q_BYTES = 2 * Q_TILE;                // both tiles of an item
+  static constexpr int K_LO = attn::BKV * 128;
+  static constexpr int K_BYTES = K_LO + attn::BKV * HI * 2;  // 8 / 10 KB
+  static constexpr int V_ROWS = 80;
+  static constexpr int V_BYTES = V_ROWS * 128;
+  static constexpr int V_TMA = HD * 128;  // bytes loaded per stage
+  static constexpr int STAGE = K_BYTES + V_BYTES;
+  static constexpr int SMEM = 1024 + attn::QBUF * Q_BYTES + attn::KV_STAGES * STAGE + 256;
+  static constexpr int O_LD = HD == 64 ? 64 : 80;  // O columns read by the epilogue (O, then l at column HD)
+};
+
+// K-major SW32 descriptor (32-byte rows, 8-row atoms of 256 B).
+__device__ __forceinline__ uint64_t sw32_kmajor_desc(uint32_t smem_addr) {
+  return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -116,11 +136,16 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       : "memory");
 }
 
+template <int HD>
 __global__ void __launch_bounds__(attn::THREADS, 1)
-    attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQh,
+                     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKh,
                      const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ out, int T, int heads,
                      int nitems) {
   using namespace attn;
+  using AC = AttnCfg<HD>;
+  constexpr int Q_TILE = AC::Q_TILE, Q_BYTES = AC::Q_BYTES, K_BYTES = AC::K_BYTES, STAGE = AC::STAGE;
+  constexpr int V_ROWS = AC::V_ROWS, V_TMA = AC::V_TMA;
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array (keeps the pointer in the shared window: LDS/STS, not generic)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -150,6 +175,10 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
+    if constexpr (AC::HI > 0) {
+      tma_prefetch(&tmQh);
+      tma_prefetch(&tmKh);
+    }
     for (int i = 0; i < QBUF; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 2);
@@ -167,10 +196,11 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<TMEM_COLS>(tmem_holder);
-  // V^T rows 64..79 of every stage: row 64 = fp16 ones (its PV output column is
-  // the softmax row sum), rows 65..79 = 0 (constant rows are swizzle-invariant).
-  for (int i = threadIdx.x; i < KV_STAGES * 16 * 8; i += blockDim.x) {
-    const int stg = i / 128, rr = i % 128 / 8, ch = i % 8;
+  // V^T rows HD..79 of every stage: row HD = fp16 ones (its PV output column is
+  // the softmax row sum), the rest 0 (constant rows are swizzle-invariant).
+  constexpr int CROWS = V_ROWS - HD;
+  for (int i = threadIdx.x; i < KV_STAGES * CROWS * 8; i += blockDim.x) {
+    const int stg = i / (CROWS * 8), rr = i % (CROWS * 8) / 8, ch = i % 8;
     const uint32_t w = rr == 0 ? 0x3C003C00u : 0u;
     *reinterpret_cast<uint4*>(sKV + stg * STAGE + K_BYTES + (HD + rr) * 128 + ch * 16) = make_uint4(w, w, w, w);
   }
@@ -189,14 +219,19 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         const int qb = local & 1;
         mbar_wait(&q_empty[qb], ((local >> 1) & 1) ^ 1);
         mbar_expect_tx(&q_full[qb], Q_BYTES);
-        tma_load_2d(sQ + qb * Q_BYTES, &tmQ, &q_full[qb], 0, bh * T + q0);
-        tma_load_2d(sQ + qb * Q_BYTES + Q_TILE, &tmQ, &q_full[qb], 0, bh * T + q0 + BQ);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          tma_load_2d(sQ + qb * Q_BYTES + t * Q_TILE, &tmQ, &q_full[qb], 0, bh * T + q0 + t * BQ);
+          if constexpr (AC::HI > 0)
+            tma_load_2d(sQ + qb * Q_BYTES + t * Q_TILE + AC::Q_LO, &tmQh, &q_full[qb], 64, bh * T + q0 + t * BQ);
+        }
         for (int j = 0; j < nkv; ++j, ++kv) {
           const int s = kv % KV_STAGES;
           mbar_wait(&kv_empty[s], ((kv / KV_STAGES) & 1) ^ 1);
           uint8_t* st = sKV + s * STAGE;
           mbar_expect_tx(&kv_full[s], K_BYTES + V_TMA);
           tma_load_2d(st, &tmK, &kv_full[s], 0, bh * T + j * BKV);
+          if constexpr (AC::HI > 0) tma_load_2d(st + AC::K_LO, &tmKh, &kv_full[s], 64, bh * T + j * BKV);
           tma_load_2d(st + K_BYTES, &tmV, &kv_full[s], j * BKV, bh * HD);
         }
       }
@@ -216,7 +251,10 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       const uint64_t kd = kv_desc0 + (uint64_t)((s * STAGE) >> 4);
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) mma_bf16_ss(tmem + S_COL(t, b), qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + S_COL(t, b), qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+        if constexpr (AC::HI > 0)  // head-dim elements 64..79 from the SW32 parts
+          mma_bf16_ss(tmem + S_COL(t, b), sw32_kmajor_desc(smem_u32(sQ + qb * Q_BYTES + t * Q_TILE + AC::Q_LO)),
+                      sw32_kmajor_desc(smem_u32(sKV + s * STAGE + AC::K_LO)), idesc_s, 1);
         mma_commit(&s_full[2 * t + b]);
       }
       __syncwarp();
@@ -344,22 +382,22 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         mbar_arrive(&p_full[2 * t + b]);
         if (lane == 0 && quarter == 0) ATR(2 * t + 1, G);
       }
-      // epilogue: O / l -> bf16 -> out[row*T + q, head*64 ...]
+      // epilogue: O / l -> bf16 -> out[row*T + q, head*HD ...]
       mbar_wait(&o_full[2 * t + 1], ((G - 1) >> 1) & 1);  // last PV (odd buffer); earlier PVs completed before it
       tc_fence_after();
-      float ov[64], lv[16];
+      float ov[80];
       tmem_ld32(o_addr, *reinterpret_cast<float(*)[32]>(&ov[0]));
       tmem_ld32(o_addr + 32, *reinterpret_cast<float(*)[32]>(&ov[32]));
-      tmem_ld16(o_addr + 64, lv);
+      tmem_ld16(o_addr + 64, *reinterpret_cast<float(*)[16]>(&ov[64]));
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&o_free[t]);
-      const float inv = 1.0f / lv[0];  // column 64 = sum_k P[r, k], exactly the P the MMA saw
+      const float inv = 1.0f / ov[HD];  // column HD = sum_k P[r, k], exactly the P the MMA saw
       const int bh = item / qpairs, q0 = (item % qpairs) * 2 * BQ;
       const int row = bh / heads, head = bh % heads;
       __nv_bfloat16* dst = out + ((int64_t)row * T + q0 + t * BQ + r) * (heads * HD) + head * HD;
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < HD / 8; ++i)
         reinterpret_cast<uint4*>(dst)[i] =
             make_uint4(pack_bf16(ov[8 * i] * inv, ov[8 * i + 1] * inv), pack_bf16(ov[8 * i + 2] * inv, ov[8 * i + 3] * inv),
                        pack_bf16(ov[8 * i + 4] * inv, ov[8 * i + 5] * inv), pack_bf16(ov[8 * i + 6] * inv, ov[8 * i + 7] * inv));
@@ -371,11 +409,20 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
   if (warp == 9) tmem_dealloc<attn::TMEM_COLS>(tmem);
 }
 
-int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T) {
+int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T,
+                   int hd) {
   const uint64_t bhT = (uint64_t)rows * heads * T;
-  if (make_tmap_bf16_2d(&m->q, q, 64, bhT, 64, 64, attn::BQ) != SF_OK) return SF_ERR_CUDA;
-  if (make_tmap_bf16_2d(&m->k, k, 64, bhT, 64, 64, attn::BKV) != SF_OK) return SF_ERR_CUDA;
-  if (make_tmap_bf16_2d(&m->v, vt, T, (uint64_t)rows * heads * 64, T, 64, 64) != SF_OK) return SF_ERR_CUDA;
+  m->hd = hd;
+  if (make_tmap_bf16_2d(&m->q, q, hd, bhT, hd, 64, attn::BQ) != SF_OK) return SF_ERR_CUDA;
+  if (make_tmap_bf16_2d(&m->k, k, hd, bhT, hd, 64, attn::BKV) != SF_OK) return SF_ERR_CUDA;
+  if (make_tmap_bf16_2d(&m->v, vt, T, (uint64_t)rows * heads * hd, T, 64, hd) != SF_OK) return SF_ERR_CUDA;
+  if (hd > 64) {  // elements 64..79 (72..79 out of bounds -> zero fill), 32-byte rows
+    if (make_tmap_bf16_2d(&m->qh, q, hd, bhT, hd, 16, attn::BQ, 32) != SF_OK) return SF_ERR_CUDA;
+    if (make_tmap_bf16_2d(&m->kh, k, hd, bhT, hd, 16, attn::BKV, 32) != SF_OK) return SF_ERR_CUDA;
+  } else {
+    m->qh = m->q;
+    m->kh = m->k;
+  }
   return SF_OK;
 }
 
@@ -390,10 +437,11 @@ static int attn_sm_count() {
   return n;
 }
 
-int prepare_attn_kernel() {
+template <int HD>
+static int prepare_attn_hd() {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_fwd_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::SMEM) !=
+    if (cudaFuncSetAttribute(attn_fwd_tcgen05<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<HD>::SMEM) !=
         cudaSuccess)
       return SF_ERR_CUDA;
     attr = true;
@@ -401,11 +449,20 @@ int prepare_attn_kernel() {
   return SF_OK;
 }
 
+int prepare_attn_kernel() { return prepare_attn_hd<64>() == SF_OK && prepare_attn_hd<72>() == SF_OK ? SF_OK : SF_ERR_CUDA; }
+
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st) {
   if (prepare_attn_kernel() != SF_OK) return SF_ERR_CUDA;
   const int64_t items = rows * heads * (T / (2 * attn::BQ));
   const int grid = (int)(items < attn_sm_count() ? items : attn_sm_count());
-  attn_fwd_tcgen05<<<grid, attn::THREADS, attn::SMEM, st>>>(m.q, m.k, m.v, out, T, heads, (int)items);
+  if (m.hd == 64)
+    attn_fwd_tcgen05<64><<<grid, attn::THREADS, AttnCfg<64>::SMEM, st>>>(m.q, m.qh, m.k, m.kh, m.v, out, T, heads,
+                                                                          (int)items);
+  else if (m.hd == 72)
+    attn_fwd_tcgen05<72><<<grid, attn::THREADS, AttnCfg<72>::SMEM, st>>>(m.q, m.qh, m.k, m.kh, m.v, out, T, heads,
+                                                                          (int)items);
+  else
+    return SF_ERR_PARAMETER;
   return cuda_status();
 }
 
@@ -417,10 +474,15 @@ extern "C" int sf_attn_trace_read(long long* dst) {
 }
 #endif
 
+extern "C" int sf_attention_hd(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads,
+                               int32_t T, int32_t hd, void* stream) {
+  if (rows < 1 || heads < 1 || T < 256 || T % 256 || (hd != 64 && hd != 72)) return SF_ERR_PARAMETER;
+  sf::AttnMaps m;
+  if (sf::make_attn_maps(&m, q, k, vt, rows, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
+  return sf::launch_attn(m, reinterpret_cast<__nv_bfloat16*>(out), rows, heads, T, (cudaStream_t)stream);
+}
+
 extern "C" int sf_attention(const void* q, const void* k, const void* vt, void* out, int64_t rows, int32_t heads,
                             int32_t T, void* stream) {
-  if (rows < 1 || heads < 1 || T < 256 || T % 256) return SF_ERR_PARAMETER;
-  sf::AttnMaps m;
-  if (sf::make_attn_maps(&m, q, k, vt, rows, heads, T) != SF_OK) return SF_ERR_CUDA;
-  return sf::launch_attn(m, reinterpret_cast<__nv_bfloat16*>(out), rows, heads, T, (cudaStream_t)stream);
+  return sf_attention_hd(q, k, vt, out, rows, heads, T, 64, stream);
 }

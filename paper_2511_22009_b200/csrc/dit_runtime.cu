@@ -553,7 +553,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
     rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
   }
-  rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
+  rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens, c.hidden / c.heads);
   if (rc != SF_OK) {
     delete h;
     return SF_ERR_CUDA;

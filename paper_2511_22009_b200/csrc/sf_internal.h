@@ -23,9 +23,11 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
                 cudaStream_t st);
 
 struct AttnMaps {
-  CUtensorMap q, k, v;
+  CUtensorMap q, qh, k, kh, v;  // qh/kh: head-dim elements 64..79 (head dim 72 only)
+  int hd;
 };
-int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T);
+int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T,
+                   int hd);
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st);
 
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }

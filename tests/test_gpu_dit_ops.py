@@ -88,3 +88,21 @@ def test_attention_matches_sdpa(rows, H, scale):
     ref = ref.permute(0, 2, 1, 3).reshape(rows * T, H * 64)
     err = (out.float() - ref).abs().max().item()
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("rows,H,scale", [(1, 16, 1.0), (2, 16, 6.0)])
+def test_attention_hd72_matches_sdpa(rows, H, scale):
+    """Head dim 72 (DiT-XL/2): QK^T zero-padded to 80 on chip, ones-row at 72."""
+    T, hd = 1024, 72
+    g = torch.Generator(device="cuda").manual_seed(7 + rows)
+    q = bf(torch.randn(rows, H, T, hd, device="cuda", generator=g) * scale / hd ** 0.5)
+    k = bf(torch.randn(rows, H, T, hd, device="cuda", generator=g))
+    v = bf(torch.randn(rows, H, T, hd, device="cuda", generator=g))
+    vt = v.transpose(-1, -2).contiguous().to(torch.float16)
+    out = torch.empty(rows * T, H * hd, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_attention_hd", q.data_ptr(), k.data_ptr(), vt.data_ptr(), out.data_ptr(), rows, H, T, hd, st())
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float(), scale=1.0)
+    ref = ref.permute(0, 2, 1, 3).reshape(rows * T, H * hd)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
