@@ -147,6 +147,18 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
  * multiplied by q_scale), V -> V^T [M/T, heads, 64, T] fp16.  K = heads*64. */
 int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,
                 int32_t T, float q_scale, void* stream);
+/* Same with head dim hd in {64, 72}: Q, K [M/T, heads, T, hd] bf16, V^T [M/T, heads, hd, T] fp16. */
+int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M,
+                   int32_t heads, int32_t T, int32_t hd, float q_scale, void* stream);
+
+/* Gated residual only (rows wider than one TMEM tile, e.g. DiT-XL hidden 1152):
+ *   xres += gate[slot] * (A . W^T + bias)     (bf16, in place); N % 128 == 0. */
+int sf_gemm_res(const void* A, const void* W, const float* bias, void* xres, const float* gate, int64_t vec_stride,
+                int64_t M, int64_t N, int64_t K, int32_t tokens_per_slot, void* stream);
+
+/* xmod = LayerNorm(xres) * (1 + scale[slot]) + shift[slot]  (no affine LN params), N in {384, 1152}. */
+int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float* scale, int64_t vec_stride,
+                   int64_t M, int64_t N, int32_t tokens_per_slot, float ln_eps, void* stream);
 
 /* Gated residual + LayerNorm + adaLN modulate fused into the GEMM epilogue:
  *   xres += gate[slot] * (A . W^T + bias)            (bf16 residual, in place)

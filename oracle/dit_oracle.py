@@ -26,7 +26,7 @@ import torch.nn.functional as F
 def timestep_features(t: torch.Tensor, dim: int = 256) -> torch.Tensor:
     """sinusoid(1000 t): cos | sin over freqs exp(-ln(1e4) k / half)."""
     half = dim // 2
-    freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float32) / half)
+    freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float32, device=t.device) / half)
     args = (1000.0 * t.to(torch.float64)).to(torch.float32)[:, None] * freqs[None]
     return torch.cat([torch.cos(args), torch.sin(args)], dim=-1)
 
@@ -65,3 +65,11 @@ def dit_forward(params: dict, x: torch.Tensor, t: torch.Tensor, emb: torch.Tenso
     out = F.linear(h, params["final_w"], params["final_b"])  # [B, T, p*p*C]
     out = out.reshape(B, gh, gw, patch, patch, Cc)
     return torch.einsum("nhwpqc->nchpwq", out).reshape(B, Cc, gh * patch, gw * patch)
+
+
+def params_to(params: dict, device) -> dict:
+    """The same parameters on another device (e.g. to run this fp32 reference on a
+    GPU for the DiT-XL/2-sized parity test, where the CPU is too slow)."""
+    out = {k: (v.to(device) if torch.is_tensor(v) else v) for k, v in params.items() if k != "blocks"}
+    out["blocks"] = [{k: v.to(device) for k, v in b.items()} for b in params["blocks"]]
+    return out

@@ -35,20 +35,49 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
-int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,
-                int32_t T, float q_scale, void* stream) {
-  const int64_t d = (int64_t)heads * 64, N = 3 * d, K = d;
-  if (M < 1 || M % T || T % 128 || N % 192 || K % 64) return SF_ERR_PARAMETER;
+int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M,
+                   int32_t heads, int32_t T, int32_t hd, float q_scale, void* stream) {
+  const int bn = hd == 64 ? 192 : 144;
+  const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
+  if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, 192) != SF_OK) return SF_ERR_CUDA;
-  if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T) != SF_OK) return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
   ep.heads = heads;
   ep.q_scale = q_scale;
   ep.tokens_per_slot = T;
   ep.M = (int)M;
-  return launch_gemm(EPI_QKV, 192, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+}
+
+int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,
+                int32_t T, float q_scale, void* stream) {
+  return sf_gemm_qkv_hd(A, W, bias, q, k, vt, M, heads, T, 64, q_scale, stream);
+}
+
+int sf_gemm_res(const void* A, const void* W, const float* bias, void* xres, const float* gate, int64_t vec_stride,
+                int64_t M, int64_t N, int64_t K, int32_t tokens_per_slot, void* stream) {
+  if (N % 128 || K % 64 || M < 1 || tokens_per_slot < 128 || M % tokens_per_slot || tokens_per_slot % 128)
+    return SF_ERR_PARAMETER;
+  GemmMaps maps;
+  if (make_operand_maps(&maps, A, M, K, W, N, 128) != SF_OK) return SF_ERR_CUDA;
+  if (make_out_map(&maps.d[0], xres, M, N) != SF_OK) return SF_ERR_CUDA;
+  EpiParams ep{};
+  ep.bias = bias;
+  ep.gate = gate;
+  ep.vec_stride = vec_stride;
+  ep.tokens_per_slot = tokens_per_slot;
+  ep.M = (int)M;
+  return launch_gemm(EPI_RES, 128, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+}
+
+int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float* scale, int64_t vec_stride,
+                   int64_t M, int64_t N, int32_t tokens_per_slot, float ln_eps, void* stream) {
+  if ((N != 384 && N != 1152) || M < 1 || tokens_per_slot < 1 || M % tokens_per_slot) return SF_ERR_PARAMETER;
+  return launch_ln_modulate((const __nv_bfloat16*)xres, (__nv_bfloat16*)xmod, shift, scale, vec_stride, M, (int)N,
+                            tokens_per_slot, ln_eps, (cudaStream_t)stream);
 }
 
 // Diagnostics only (not in the header): 1 = skip epilogue stores, 2 = main loop only.

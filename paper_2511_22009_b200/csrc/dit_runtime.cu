@@ -85,24 +85,23 @@ __global__ void cond_kernel(RowSrc src, int hidden, int freq_dim, const __nv_bfl
   } else {
     er = src.emb + i * src.E;
   }
-  const int n = threadIdx.x;
   const int half = freq_dim / 2;
   const float tm = (float)(1000.0 * t);
-  for (int k = n; k < half; k += blockDim.x) {
+  for (int k = threadIdx.x; k < half; k += blockDim.x) {
     const float fr = expf(-9.210340371976184f * (float)k / (float)half);  // ln(10000)
     const float a = tm * fr;
     f[k] = cosf(a);
     f[half + k] = sinf(a);
   }
-  for (int k = n; k < src.E; k += blockDim.x) e[k] = zero_emb ? 0.0f : (float)er[k];
+  for (int k = threadIdx.x; k < src.E; k += blockDim.x) e[k] = zero_emb ? 0.0f : (float)er[k];
   __syncthreads();
-  if (n < hidden) {
+  for (int n = threadIdx.x; n < hidden; n += blockDim.x) {
     float acc = b1[n];
     for (int k = 0; k < freq_dim; ++k) acc += f[k] * __bfloat162float(w1t[(int64_t)k * hidden + n]);
     h1[n] = silu(acc);
   }
   __syncthreads();
-  if (n < hidden) {
+  for (int n = threadIdx.x; n < hidden; n += blockDim.x) {
     float acc = b2[n];
     for (int k = 0; k < hidden; ++k) acc += h1[k] * __bfloat162float(w2t[(int64_t)k * hidden + n]);
     float y = yb[n];
@@ -195,6 +194,72 @@ __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
       *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
     }
   }
+}
+
+// ============================================================ K4: LayerNorm + adaLN modulate (wide rows)
+// xmod = LN(xres) * (1 + scale[slot]) + shift[slot]; one warp per token, lane
+// owns columns 128u + 4 lane + {0..3}.  Used where the row is wider than one
+// TMEM accumulator tile (DiT-XL hidden 1152), after the gated-residual GEMM.
+template <int HID>
+__global__ void __launch_bounds__(256) ln_modulate_kernel(const __nv_bfloat16* __restrict__ xres,
+                                                          __nv_bfloat16* __restrict__ xmod,
+                                                          const float* __restrict__ shift,
+                                                          const float* __restrict__ scale, int64_t vec_stride,
+                                                          int64_t M, int T, float ln_eps) {
+  constexpr int U = HID / 128;
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < M; tok += wstride) {
+    float y[U][4];
+    float sum = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(xres + tok * HID + 128 * u + 4 * lane);
+      const float2 a = unpack_bf16(raw.x), b = unpack_bf16(raw.y);
+      y[u][0] = a.x;
+      y[u][1] = a.y;
+      y[u][2] = b.x;
+      y[u][3] = b.y;
+      sum += (a.x + a.y) + (b.x + b.y);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / HID;
+    float var = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float rstd = rsqrtf(var / HID + ln_eps);
+    const int64_t slot = tok / T;
+    const float* sh = shift + slot * vec_stride;
+    const float* sc = scale + slot * vec_stride;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int n0 = 128 * u + 4 * lane;
+      const float4 s4 = *reinterpret_cast<const float4*>(sh + n0);
+      const float4 c4 = *reinterpret_cast<const float4*>(sc + n0);
+      const float o0 = (y[u][0] - mean) * rstd * (1.0f + c4.x) + s4.x;
+      const float o1 = (y[u][1] - mean) * rstd * (1.0f + c4.y) + s4.y;
+      const float o2 = (y[u][2] - mean) * rstd * (1.0f + c4.z) + s4.z;
+      const float o3 = (y[u][3] - mean) * rstd * (1.0f + c4.w) + s4.w;
+      *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+    }
+  }
+}
+
+int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const float* shift, const float* scale,
+                       int64_t vec_stride, int64_t M, int N, int tokens_per_slot, float eps, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16);
+  if (N == 384)
+    ln_modulate_kernel<384><<<blocks, 256, 0, st>>>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps);
+  else if (N == 1152)
+    ln_modulate_kernel<1152><<<blocks, 256, 0, st>>>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps);
+  else
+    return SF_ERR_PARAMETER;
+  return cuda_status();
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
@@ -407,61 +472,64 @@ static int run_forward_core(sf_dit* h, int64_t rows, cudaStream_t st) {
 
 static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
-  const int H = c.hidden, T = h->tokens;
+  const int H = c.hidden, T = h->tokens, hd = H / c.heads;
   const int64_t M = rows * T;
   const int64_t B6 = 6 * (int64_t)H;
+  // hidden 384: the 384-wide row fits one TMEM tile, so the gated residual and the
+  // next LayerNorm + modulate run in the GEMM epilogue (RES_LN).  Wider rows
+  // (DiT-XL, 1152): gated-residual epilogue (RES) + a LayerNorm/modulate pass.
+  const bool fused_ln = H == 384;
   int rc;
   for (int l = 0; l < c.depth; ++l) {
     {
       EpiParams ep{};
       ep.bias = h->w.qkv_b + (int64_t)l * 3 * H;
       ep.heads = c.heads;
-      ep.q_scale = 0.125f;  // 1/sqrt(64)
+      ep.q_scale = 1.0f / sqrtf((float)hd);
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_QKV, 192, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_QKV, hd == 64 ? 192 : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
       mark(h, P_QKV, st);
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
     mark(h, P_ATTN, st);
-    {
+    for (int half = 0; half < 2; ++half) {  // 0: attention proj (gate_msa), 1: MLP (fc1 + GELU, fc2, gate_mlp)
+      if (half == 1) {
+        EpiParams ep{};
+        ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
+        ep.ldo = c.mlp_hidden;
+        ep.tokens_per_slot = T;
+        ep.M = (int)M;
+        if ((rc = launch_gemm(EPI_GELU, 256, h->g_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
+        mark(h, P_FC1, st);
+      }
+      const GemmMaps& gm = half == 0 ? h->g_proj[l] : h->g_fc2[l];
+      const int K = half == 0 ? H : c.mlp_hidden;
+      const int cls = half == 0 ? P_PROJ : P_FC2;
       EpiParams ep{};
-      ep.bias = h->w.proj_b + (int64_t)l * H;
+      ep.bias = (half == 0 ? h->w.proj_b : h->w.fc2_b) + (int64_t)l * H;
       ep.xres = h->xres;
-      ep.gate = h->mod + l * B6 + 2 * H;   // gate_msa
-      ep.shift = h->mod + l * B6 + 3 * H;  // shift_mlp
-      ep.scale = h->mod + l * B6 + 4 * H;  // scale_mlp
-      ep.vec_stride = h->mod_stride;
-      ep.ln_eps = c.ln_eps;
-      ep.tokens_per_slot = T;
-      ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_RES_LN, 384, h->g_proj[l], (int)M, H, H, ep, st))) return rc;
-      mark(h, P_PROJ, st);
-    }
-    {
-      EpiParams ep{};
-      ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
-      ep.ldo = c.mlp_hidden;
-      ep.tokens_per_slot = T;
-      ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_GELU, 256, h->g_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
-      mark(h, P_FC1, st);
-    }
-    {
-      EpiParams ep{};
-      ep.bias = h->w.fc2_b + (int64_t)l * H;
-      ep.xres = h->xres;
-      ep.gate = h->mod + l * B6 + 5 * H;  // gate_mlp
-      const float* nxt = (l + 1 < c.depth) ? h->mod + (l + 1) * B6  // next block: shift_msa, scale_msa
-                                           : h->mod + c.depth * B6;  // final layer: shift, scale
+      ep.gate = h->mod + l * B6 + (half == 0 ? 2 : 5) * H;  // gate_msa / gate_mlp
+      // LayerNorm modulate for what comes next: the MLP (shift_mlp, scale_mlp), the
+      // next block (shift_msa, scale_msa) or the final layer (shift, scale)
+      const float* nxt = half == 0 ? h->mod + l * B6 + 3 * H
+                                   : (l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6);
       ep.shift = nxt;
       ep.scale = nxt + H;
       ep.vec_stride = h->mod_stride;
       ep.ln_eps = c.ln_eps;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_RES_LN, 384, h->g_fc2[l], (int)M, H, c.mlp_hidden, ep, st))) return rc;
-      mark(h, P_FC2, st);
+      if (fused_ln) {
+        if ((rc = launch_gemm(EPI_RES_LN, 384, gm, (int)M, H, K, ep, st))) return rc;
+        mark(h, cls, st);
+      } else {
+        if ((rc = launch_gemm(EPI_RES, 128, gm, (int)M, H, K, ep, st))) return rc;
+        mark(h, cls, st);
+        if ((rc = launch_ln_modulate(h->xres, h->xmod, nxt, nxt + H, h->mod_stride, M, H, T, c.ln_eps, st)))
+          return rc;
+        mark(h, cls, st);
+      }
     }
   }
   return SF_OK;
@@ -470,7 +538,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
 static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const size_t sm = (c.freq_dim + c.hidden + c.embed_dim) * sizeof(float);
-  cond_kernel<<<(unsigned)rows, c.hidden, sm, st>>>(src, c.hidden, c.freq_dim, (const __nv_bfloat16*)h->w.t_w1t,
+  cond_kernel<<<(unsigned)rows, 384, sm, st>>>(src, c.hidden, c.freq_dim, (const __nv_bfloat16*)h->w.t_w1t,
                                                      h->w.t_b1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2,
                                                      (const __nv_bfloat16*)h->w.y_wt, h->w.y_b, h->cond);
   mark(h, P_COND, st);
@@ -482,10 +550,9 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   const int64_t tokens = rows * h->tokens;
   const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8);
-  patch_embed_ln_kernel<384><<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch,
-                                                      (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b,
-                                                      h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres,
-                                                      h->xmod, tokens);
+  auto kern = c.hidden == 384 ? patch_embed_ln_kernel<384> : patch_embed_ln_kernel<1152>;
+  kern<<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
+                                h->w.patch_b, h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens);
   mark(h, P_PATCH, st);
   return cuda_status();
 }
@@ -506,9 +573,11 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
                   int64_t ws_bytes, sf_dit** out) {
   if (!cfg || !w || !out || max_rows < 1) return SF_ERR_PARAMETER;
   const sf_dit_config& c = *cfg;
-  if (c.hidden != 384 || c.heads * 64 != c.hidden || c.patch != 2 || c.in_ch != 4 || c.latent_hw % 32 ||
-      c.mlp_hidden != 4 * c.hidden || c.freq_dim % 2 || c.embed_dim < 1 || c.embed_dim > 64)
-    return SF_ERR_PARAMETER;  // this build's kernels are specialised for hidden 384 / head dim 64 / patch 2
+  // kernels exist for DiT-S/2 (hidden 384, head dim 64) and DiT-XL/2 (hidden 1152, head dim 72), patch 2
+  const bool s2 = c.hidden == 384 && c.heads == 6, xl2 = c.hidden == 1152 && c.heads == 16;
+  if (!(s2 || xl2) || c.patch != 2 || c.in_ch != 4 || c.latent_hw % 32 || c.mlp_hidden != 4 * c.hidden ||
+      c.freq_dim % 2 || c.freq_dim > 1024 || c.embed_dim < 1 || c.embed_dim > 64 || c.depth < 1)
+    return SF_ERR_PARAMETER;
   int64_t off[9];
   if (ws_layout(c, max_rows, off) > ws_bytes) return SF_ERR_PARAMETER;
   auto* h = new sf_dit();
@@ -542,16 +611,24 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     const __nv_bfloat16* proj = (const __nv_bfloat16*)w->proj_w + (int64_t)l * H * H;
     const __nv_bfloat16* fc1 = (const __nv_bfloat16*)w->fc1_w + (int64_t)l * c.mlp_hidden * H;
     const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
-    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, 192);
-    rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens);
-    rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
-    rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);
-    rc |= make_out_map32(&h->g_proj[l].d[1], h->xmod, M, H);
+    const int hd = H / c.heads;
+    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? 192 : 144);
+    rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
     rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
     rc |= make_out_map(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);
-    rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 384);
-    rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
-    rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
+    if (H == 384) {  // RES_LN epilogue: whole rows per tile
+      rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
+      rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);
+      rc |= make_out_map32(&h->g_proj[l].d[1], h->xmod, M, H);
+      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 384);
+      rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
+      rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
+    } else {  // RES epilogue (128-wide tiles) + LayerNorm pass
+      rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 128);
+      rc |= make_out_map(&h->g_proj[l].d[0], h->xres, M, H);
+      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 128);
+      rc |= make_out_map(&h->g_fc2[l].d[0], h->xres, M, H);
+    }
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens, c.hidden / c.heads);
   if (rc != SF_OK) {
@@ -563,12 +640,13 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     delete h;
     return SF_ERR_CUDA;
   }
-  cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)));
-  cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)final_smem(c));
-  cudaFuncSetAttribute(final_layer_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)final_smem(c));
+  const int psm = (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)), fsm = (int)final_smem(c);
+  cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+  cudaFuncSetAttribute(patch_embed_ln_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+  cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+  cudaFuncSetAttribute(final_layer_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+  cudaFuncSetAttribute(final_layer_kernel<1152, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+  cudaFuncSetAttribute(final_layer_kernel<1152, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   *out = h;
   return cuda_status();
 }
@@ -593,7 +671,8 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if ((rc = launch_patch(h, x, rows, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = rows * h->tokens;
-  final_layer_kernel<384, false><<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
+  auto fk = c.hidden == 384 ? final_layer_kernel<384, false> : final_layer_kernel<1152, false>;
+  fk<<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, rows, eps_out,
       nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr, tokens);
   return cuda_status();
@@ -616,7 +695,8 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = R * h->tokens;
-  final_layer_kernel<384, true><<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
+  auto fk = c.hidden == 384 ? final_layer_kernel<384, true> : final_layer_kernel<1152, true>;
+  fk<<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
       m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
   mark(h, P_FINAL, st);

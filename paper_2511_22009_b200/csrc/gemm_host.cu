@@ -63,18 +63,30 @@ int make_out_map32(CUtensorMap* m, const void* D, int64_t rows, int64_t cols) {
   return make_tmap_bf16_2d(m, D, cols, rows, cols, 32, 32, 64);
 }
 
-// QKV outputs: Q, K [rows*H*T, 64] and V^T [rows*H*64, T] (32-token x 64-dim chunks, 64B swizzle).
-int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T) {
+// QKV outputs: Q, K [rows*H*T, hd] and V^T [rows*H*hd, T].
+//   hd 64: 32-token x 64-dim chunks (Q/K 128B swizzle, V^T 64B swizzle)
+//   hd 72: whole heads, Q/K box 72 x 32 unswizzled (144-byte rows), V^T box 32 x 72 (64B swizzle)
+int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T,
+                      int hd) {
   const int64_t bh = rows * heads;
-  int rc = make_tmap_bf16_2d(&m->d[0], q, 64, bh * T, 64, 64, 32, 128);
-  rc |= make_tmap_bf16_2d(&m->d[1], k, 64, bh * T, 64, 64, 32, 128);
-  rc |= make_tmap_bf16_2d(&m->d[2], vt, T, bh * 64, T, 32, 64, 64);
+  int rc;
+  if (hd == 64) {
+    rc = make_tmap_bf16_2d(&m->d[0], q, 64, bh * T, 64, 64, 32, 128);
+    rc |= make_tmap_bf16_2d(&m->d[1], k, 64, bh * T, 64, 64, 32, 128);
+    rc |= make_tmap_bf16_2d(&m->d[2], vt, T, bh * 64, T, 32, 64, 64);
+  } else if (hd == 72) {
+    rc = make_tmap_bf16_2d(&m->d[0], q, 72, bh * T, 72, 72, 32, 0);
+    rc |= make_tmap_bf16_2d(&m->d[1], k, 72, bh * T, 72, 72, 32, 0);
+    rc |= make_tmap_bf16_2d(&m->d[2], vt, T, bh * 72, T, 32, 72, 64);
+  } else {
+    return SF_ERR_PARAMETER;
+  }
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
 template <int BN, int KIND>
 constexpr int epi_warps() {
-  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;
+  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;  // EPI_RES: 8
 }
 
 template <int BN, int KIND>
@@ -105,6 +117,8 @@ int prepare_gemm_kernels() {
   rc |= set_attr<256, EPI_GELU>();
   rc |= set_attr<192, EPI_QKV>();
   rc |= set_attr<384, EPI_RES_LN>();
+  rc |= set_attr<144, EPI_QKV>();
+  rc |= set_attr<128, EPI_RES>();
   return rc;
 }
 
@@ -152,6 +166,8 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
   SF_CASE(256, EPI_GELU)
   SF_CASE(192, EPI_QKV)
   SF_CASE(384, EPI_RES_LN)
+  SF_CASE(144, EPI_QKV)
+  SF_CASE(128, EPI_RES)
 #undef SF_CASE
   return SF_ERR_PARAMETER;
 }

@@ -26,6 +26,7 @@ enum EpiKind : int {
   EPI_GELU = 2,    // out bf16 [M, ldo] = gelu_tanh(acc + bias)
   EPI_QKV = 3,     // scatter to Q,K [rows, H, T, 64] bf16 and V^T [rows, H, 64, T] fp16; Q pre-scaled
   EPI_RES_LN = 4,  // x += gate*(acc+bias) (bf16 residual); xmod = LN(x)*(1+scale)+shift
+  EPI_RES = 5,     // x += gate*(acc+bias) only (wide rows; LayerNorm runs as its own pass)
 };
 
 struct EpiParams {
@@ -77,7 +78,8 @@ struct GemmCfg {
   // per-warp output staging, double-buffered: 32 rows x 128 B (SW128), or 32 x 64 B (SW64) with 12 warps
   // (RES_LN: a 3-deep ring per warp; residual chunks are TMA-loaded into it and
   // overwritten in place by the updated residual before its TMA store)
-  static constexpr int OUT_BUF = EPI_WARPS == 12 ? 2048 : 4096;
+  // (head dim 72 QKV, BN = 144: 32 x 144 B Q/K rows or 72 x 64 B V^T rows per buffer)
+  static constexpr int OUT_BUF = BN == 144 ? 5120 : EPI_WARPS == 12 ? 2048 : 4096;
   static constexpr int OUT_NBUF = EPI_WARPS == 12 ? 3 : 2;
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
   static constexpr int RBAR_BYTES = EPI_WARPS * 3 * 8;  // residual-chunk barriers (RES_LN ring)
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS * 32);
     }
-    if constexpr (KIND == EPI_RES_LN)
+    if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES)
       for (int i = 0; i < EPI_WARPS * 3; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
@@ -267,6 +269,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       float* vb = vecs + (local & 1) * (4 * BN);
       for (int c = et; c < BN; c += EPI_THREADS) {
         vb[c] = ep.bias[n0 + c];
+        if constexpr (KIND == EPI_RES) vb[BN + c] = ep.gate[(int64_t)slot * ep.vec_stride + n0 + c];
         if constexpr (KIND == EPI_RES_LN) {
           const int64_t o = (int64_t)slot * ep.vec_stride + n0 + c;
           vb[BN + c] = ep.gate[o];
@@ -288,6 +291,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           bulk_wait_read<1>();  // the previous users of these two buffers (stores) have read them
           res_load(ring, 0);
           res_load(ring + 1, 1);
+        }
+        __syncwarp();
+      }
+      // RES (wide rows): the residual chunks of this thread's columns (64 at a
+      // time, SW128 staging) are TMA-loaded into the warp's two staging buffers.
+      if constexpr (KIND == EPI_RES) {
+        static_assert(KIND != EPI_RES || COLS <= 128, "RES: at most two 64-column chunks per warp");
+        if (lane == 0) {
+          bulk_wait_read<0>();  // previous tile's stores have read both buffers
+#pragma unroll
+          for (int c = 0; c < COLS / 64; ++c) {
+            mbar_expect_tx(&rbar[e * 3 + c], 4096);
+            tma_load_2d(rbuf0 + c * 4096, &maps.d[0], &rbar[e * 3 + c], n0 + c_lo + 64 * c, r0);
+          }
         }
         __syncwarp();
       }
@@ -349,6 +366,93 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           }
           out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
         }
+      } else if constexpr (KIND == EPI_QKV && BN == 144) {
+        // head dim 72: a 144-column tile = two whole heads of one of Q / K / V.
+        // Q, K rows (72 bf16 = 144 B) staged unswizzled, box 72 x 32; V^T staged as
+        // 72 head-dim rows x 32 tokens (fp16, 64-byte rows, 64B swizzle).
+        const int d = ep.heads * 72;
+        const int T = ep.tokens_per_slot;
+        const int tok0 = r0 - slot * T;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          const int gc = n0 + 72 * hh;
+          const int which = gc / d;
+          const int head = (gc - which * d) / 72;
+          const int64_t hb = ((int64_t)slot * ep.heads + head);
+          const float sc = which == 0 ? ep.q_scale : 1.0f;
+          uint8_t* buf = out.acquire(lane);
+          float v[80];
+          tmem_ld32(taddr + 72 * hh, *reinterpret_cast<float(*)[32]>(&v[0]));
+          tmem_ld32(taddr + 72 * hh + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
+          tmem_ld16(taddr + 72 * hh + 64, *reinterpret_cast<float(*)[16]>(&v[64]));
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+#pragma unroll
+          for (int i = 0; i < 18; ++i) {
+            const float4 b = reinterpret_cast<const float4*>(vbias + 72 * hh)[i];
+            v[4 * i] = (v[4 * i] + b.x) * sc;
+            v[4 * i + 1] = (v[4 * i + 1] + b.y) * sc;
+            v[4 * i + 2] = (v[4 * i + 2] + b.z) * sc;
+            v[4 * i + 3] = (v[4 * i + 3] + b.w) * sc;
+          }
+          if (which < 2) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) *reinterpret_cast<uint4*>(buf + lane * 144 + 16 * i) = pack8_bf16(v + 8 * i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 72; ++i)
+              *reinterpret_cast<__half*>(buf + i * 64 + ((((lane >> 3) ^ ((i >> 1) & 3))) * 16) + (lane & 7) * 2) =
+                  __float2half_rn(v[i]);
+          }
+          if (which < 2)
+            out.release(lane, &maps.d[which], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          else
+            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 72), do_store && r0 < ep.M);
+        }
+      } else if constexpr (KIND == EPI_RES) {
+        const float* vgate = vb + BN + c_lo;
+        const bool st_ok = do_store && r0 < ep.M;
+#pragma unroll 1
+        for (int c = 0; c < COLS / 64; ++c) {
+          uint8_t* buf = rbuf0 + c * 4096;
+          mbar_wait(&rbar[e * 3 + c], (ring >> c) & 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            tmem_ld32(taddr + c_lo + 64 * c + 32 * h, v);
+            tmem_ld_wait();
+            if (c + 1 == COLS / 64 && h == 1) {
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint4* slotp = reinterpret_cast<uint4*>(buf + lane * 128 + (((4 * h + i) ^ (lane & 7)) * 16));
+              const uint4 o = *slotp;
+              const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+              uint32_t nw[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int col = 64 * c + 32 * h + 8 * i + 2 * k;
+                const float2 x0 = unpack_bf16(ow[k]);
+                nw[k] = pack_bf16(x0.x + vgate[col] * (v[8 * i + 2 * k] + vbias[col]),
+                                  x0.y + vgate[col + 1] * (v[8 * i + 2 * k + 1] + vbias[col + 1]));
+              }
+              *slotp = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (st_ok) tma_store_2d(&maps.d[0], buf, n0 + c_lo + 64 * c, r0);
+            bulk_commit();
+          }
+          __syncwarp();
+        }
+        ring ^= (1u << (COLS / 64)) - 1;  // per-buffer load parity
       } else if constexpr (KIND == EPI_QKV) {
         // columns [0, d) -> Q, [d, 2d) -> K, [2d, 3d) -> V; 64 columns per head
         const int d = ep.heads * 64;
