@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--n", type=int, default=4, help="steps per generation (slots per stream)")
     ap.add_argument("--windows", type=int, default=4, help="time windows K of the scheduler")
     ap.add_argument("--guidance", type=float, default=1.0)
+    ap.add_argument("--model", default="s2", choices=["s2", "xl2"],
+                    help="s2: DiT-S/2 (configs[1]); xl2: DiT-XL/2 (configs[3], 8-slot batch = 2 streams x 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -57,11 +59,24 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+MODELS = {
+    "s2": ("DiT-S/2", "DiT-S/2 (depth 12, hidden 384, 6 heads, patch 2, 1024 tokens)"),
+    "xl2": ("DiT-XL/2", "DiT-XL/2 (depth 28, hidden 1152, 16 heads of 72, patch 2, 1024 tokens)"),
+}
+
+
+def model_cfg(args):
+    from paper_2511_22009_b200.dit import DIT_S2, DIT_XL2
+
+    return DIT_XL2 if args.model == "xl2" else DIT_S2
+
+
 def workload(args, world):
+    name, desc = MODELS[args.model]
     return {
-        "workload": "DiT-S/2 random-init velocity field, 64x64x4 latent (512^2), "
+        "workload": f"{name} random-init velocity field, 64x64x4 latent (512^2), "
                     f"{args.n}-step heterogeneous stream batch, {args.streams} streams/GPU x {args.n} slots",
-        "model": "DiT-S/2 (depth 12, hidden 384, 6 heads, patch 2, 1024 tokens)",
+        "model": desc,
         "streams_per_gpu": args.streams,
         "streams_total": args.streams * world,
         "slots_per_gpu": args.streams * args.n,
@@ -137,12 +152,13 @@ def run_reference(args):
     import torch
 
     from oracle.cpu_bench import CpuStream
-    from paper_2511_22009_b200.dit import DIT_S2, init_dit_params
+    from paper_2511_22009_b200.dit import init_dit_params
 
+    cfg = model_cfg(args)
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    params = init_dit_params(DIT_S2, seed=0)
-    cs = CpuStream(params, DIT_S2.heads, n=args.n, num_windows=args.windows, w=args.guidance, seed=1000)
+    params = init_dit_params(cfg, seed=0)
+    cs = CpuStream(params, cfg.heads, n=args.n, num_windows=args.windows, w=args.guidance, seed=1000)
     for _ in range(args.warmup):
         cs.iteration()
     times = []
@@ -154,7 +170,7 @@ def run_reference(args):
     total = time.perf_counter() - t_all
     value = args.steps / total  # one frame retires per iteration of one stream
     lat = [1e3 * sum(times[i:i + args.n]) for i in range(max(1, len(times) - args.n + 1))]
-    sample = (f"1 stream x {args.n} slots per step (steady state), DiT-S/2 torch fp32 CPU oracle port, "
+    sample = (f"1 stream x {args.n} slots per step (steady state), {MODELS[args.model][0]} torch fp32 CPU oracle port, "
               f"{args.steps} steps; streams are independent so frames/s scales per stream")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
@@ -172,6 +188,8 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
+    if args.model == "xl2" and "--streams" not in sys.argv:
+        args.streams = 2  # configs[3]: 8-slot stream batch (2 streams x 4 slots) per GPU
     if args.impl == "reference":
         return run_reference(args)
     args.warmup = max(args.warmup, 3, args.n)
@@ -186,9 +204,8 @@ def main():
 
     build()
     import paper_2511_22009_b200 as sf
-    from paper_2511_22009_b200.dit import DIT_S2
 
-    cfg = DIT_S2
+    cfg = model_cfg(args)
     S, n, w = args.streams, args.n, args.guidance
     rows = S * n * (2 if w != 1.0 else 1)
     model = sf.DiTVelocityModel(cfg, seed=0, max_rows=rows)
@@ -292,14 +309,14 @@ def main():
                                   w=w, seed=1000)
         cpu = {"value": r["frames_per_s"], "unit": "frames/s", "cores": r["threads"], "kind": "port",
                "sample": f"1 stream x {n} slots, 2 timed steady-state iterations (+1 warm-up) of the torch-fp32 "
-                         "DiT-S/2 oracle port + numpy Euler step"}
+                         f"{MODELS[args.model][0]} oracle port + numpy Euler step"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (N(0,1) latents from on-device Philox, random-init DiT-S/2 weights)",
+            "data": f"synthetic (N(0,1) latents from on-device Philox, random-init {MODELS[args.model][0]} weights)",
             "config": workload(args, world),
             "p50_latency_ms": p50, "p99_latency_ms": p99,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": S * cfg.dim * 4,

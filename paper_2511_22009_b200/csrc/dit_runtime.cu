@@ -60,31 +60,58 @@ struct RowSrc {
 };
 
 // ============================================================ K1: conditioning
-// c = MLP(sinusoid(1000 t)) + Linear(emb); out = bf16(SiLU(c)) (adaLN input)
-__global__ void cond_kernel(RowSrc src, int hidden, int freq_dim, const __nv_bfloat16* __restrict__ w1t,
-                            const float* __restrict__ b1, const __nv_bfloat16* __restrict__ w2t,
-                            const float* __restrict__ b2, const __nv_bfloat16* __restrict__ ywt,
-                            const float* __restrict__ yb, __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float sh[];
-  float* f = sh;                // [freq_dim]
-  float* h1 = sh + freq_dim;    // [hidden]
-  float* e = h1 + hidden;       // [E]
-  const int64_t i = blockIdx.x;  // net row
+// c = MLP(sinusoid(1000 t)) + Linear(emb); out = bf16(SiLU(c)) (adaLN input).
+// Two launches, grid (net rows, hidden / 128), one output feature per thread,
+// weights in the transposed [in][out] layout so a warp's loads are coalesced:
+//   cond_h1_kernel:  h1 = SiLU(W1 . sinusoid(1000 t) + b1)            (fp32 scratch)
+//   cond_out_kernel: out = bf16(SiLU(W2 . h1 + b2 + Wy . emb + by))
+__device__ __forceinline__ const double* cond_emb_row(const RowSrc& src, int64_t i, bool* zero_emb) {
   const int64_t lr = i % src.R;
-  const double t = src.ts[lr];
-  const double* er;
-  bool zero_emb = false;
+  *zero_emb = false;
   if (src.row_info) {
     const int64_t s = src.row_info[lr * 4 + 3];
     if (src.cfg && i < src.R) {
-      er = src.neg ? src.neg + s * src.E : nullptr;
-      zero_emb = src.neg == nullptr;
-    } else {
-      er = src.emb + s * src.E;
+      *zero_emb = src.neg == nullptr;
+      return src.neg ? src.neg + s * src.E : nullptr;
     }
-  } else {
-    er = src.emb + i * src.E;
+    return src.emb + s * src.E;
   }
+  return src.emb + i * src.E;
+}
+
+// Block = 8 warps x 32 output features: lane = feature (coalesced 64-byte weight
+// rows), warp w reduces k in [w K/8, (w+1) K/8) with 8 loads in flight, then the
+// 8 partial sums meet in shared memory.
+__device__ __forceinline__ float dot_col_split(const float* __restrict__ v, const __nv_bfloat16* __restrict__ wt,
+                                               int K, int ld, int n, float* red) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k0 = (int)((int64_t)K * w / 8), k1 = (int)((int64_t)K * (w + 1) / 8);
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int k = k0;
+  if (n < ld) {
+    for (; k + 8 <= k1; k += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += v[k + u] * __bfloat162float(wt[(int64_t)(k + u) * ld + n]);
+    for (; k < k1; ++k) a[0] += v[k] * __bfloat162float(wt[(int64_t)k * ld + n]);
+  }
+  red[w * 32 + lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  __syncthreads();
+  float r = 0.f;
+  if (w == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r += red[q * 32 + lane];
+  __syncthreads();
+  return r;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(256) cond_h1_kernel(RowSrc src, int hidden, int freq_dim,
+                                                      const __nv_bfloat16* __restrict__ w1t,
+                                                      const float* __restrict__ b1, float* __restrict__ h1) {
+  extern __shared__ float sh[];
+  float* f = sh;               // [freq_dim]
+  float* red = sh + freq_dim;  // [8][32]
+  const int64_t i = blockIdx.x;
+  const double t = src.ts[i % src.R];
   const int half = freq_dim / 2;
   const float tm = (float)(1000.0 * t);
   for (int k = threadIdx.x; k < half; k += blockDim.x) {
@@ -93,20 +120,33 @@ __global__ void cond_kernel(RowSrc src, int hidden, int freq_dim, const __nv_bfl
     f[k] = cosf(a);
     f[half + k] = sinf(a);
   }
+  __syncthreads();
+  const int n = blockIdx.y * 32 + (threadIdx.x & 31);
+  const float acc = dot_col_split(f, w1t, freq_dim, hidden, n, red);
+  if (threadIdx.x < 32 && n < hidden) h1[i * hidden + n] = silu(b1[n] + acc);
+}
+
+__global__ void __launch_bounds__(256) cond_out_kernel(RowSrc src, int hidden, const float* __restrict__ h1g,
+                                                       const __nv_bfloat16* __restrict__ w2t,
+                                                       const float* __restrict__ b2,
+                                                       const __nv_bfloat16* __restrict__ ywt,
+                                                       const float* __restrict__ yb, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float sh[];
+  float* h1 = sh;             // [hidden]
+  float* e = sh + hidden;     // [64]
+  float* red = e + 64;        // [8][32]
+  const int64_t i = blockIdx.x;
+  bool zero_emb;
+  const double* er = cond_emb_row(src, i, &zero_emb);
+  for (int k = threadIdx.x; k < hidden; k += blockDim.x) h1[k] = h1g[i * hidden + k];
   for (int k = threadIdx.x; k < src.E; k += blockDim.x) e[k] = zero_emb ? 0.0f : (float)er[k];
   __syncthreads();
-  for (int n = threadIdx.x; n < hidden; n += blockDim.x) {
-    float acc = b1[n];
-    for (int k = 0; k < freq_dim; ++k) acc += f[k] * __bfloat162float(w1t[(int64_t)k * hidden + n]);
-    h1[n] = silu(acc);
-  }
-  __syncthreads();
-  for (int n = threadIdx.x; n < hidden; n += blockDim.x) {
-    float acc = b2[n];
-    for (int k = 0; k < hidden; ++k) acc += h1[k] * __bfloat162float(w2t[(int64_t)k * hidden + n]);
+  const int n = blockIdx.y * 32 + (threadIdx.x & 31);
+  const float acc = dot_col_split(h1, w2t, hidden, hidden, n, red);
+  if (threadIdx.x < 32 && n < hidden) {
     float y = yb[n];
     for (int k = 0; k < src.E; ++k) y += e[k] * __bfloat162float(ywt[(int64_t)k * hidden + n]);
-    out[i * hidden + n] = __float2bfloat16_rn(silu(acc + y));
+    out[i * hidden + n] = __float2bfloat16_rn(silu(b2[n] + acc + y));
   }
 }
 
@@ -397,6 +437,7 @@ struct sf_dit {
   // workspace carve-out
   __nv_bfloat16 *cond, *xres, *xmod, *q, *k, *vt, *attn, *hmid;
   float* mod;
+  float* h1;  // conditioning MLP hidden
   // TMA descriptors
   GemmMaps g_ada;                                  // TMA descriptors per GEMM call site
   std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
@@ -414,7 +455,7 @@ struct sf_dit {
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[9]*/) {
+static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[10]*/) {
   const int64_t T = (int64_t)(c.latent_hw / c.patch) * (c.latent_hw / c.patch);
   const int64_t M = rows * T, H = c.hidden;
   const int64_t mod_stride = (int64_t)c.depth * 6 * H + 2 * H;
@@ -433,6 +474,7 @@ static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[9
   take(6, M * H * 2);                 // vt
   take(7, M * H * 2);                 // attn out
   take(8, M * (int64_t)c.mlp_hidden * 2);  // mlp hidden
+  take(9, rows * H * 4);                   // conditioning MLP hidden (fp32)
   return o;
 }
 
@@ -537,10 +579,14 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
 
 static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
-  const size_t sm = (c.freq_dim + c.hidden + c.embed_dim) * sizeof(float);
-  cond_kernel<<<(unsigned)rows, 384, sm, st>>>(src, c.hidden, c.freq_dim, (const __nv_bfloat16*)h->w.t_w1t,
-                                                     h->w.t_b1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2,
-                                                     (const __nv_bfloat16*)h->w.y_wt, h->w.y_b, h->cond);
+  const dim3 grid((unsigned)rows, (unsigned)((c.hidden + 31) / 32));
+  cond_h1_kernel<<<grid, 256, (c.freq_dim + 256) * sizeof(float), st>>>(src, c.hidden, c.freq_dim,
+                                                                        (const __nv_bfloat16*)h->w.t_w1t, h->w.t_b1,
+                                                                        h->h1);
+  mark(h, P_COND, st);
+  cond_out_kernel<<<grid, 256, (c.hidden + 64 + 256) * sizeof(float), st>>>(
+      src, c.hidden, h->h1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2, (const __nv_bfloat16*)h->w.y_wt, h->w.y_b,
+      h->cond);
   mark(h, P_COND, st);
   return cuda_status();
 }
@@ -565,7 +611,7 @@ static size_t final_smem(const sf_dit_config& c) {
 extern "C" {
 
 int64_t sf_dit_workspace_bytes(const sf_dit_config* cfg, int64_t max_rows) {
-  int64_t off[9];
+  int64_t off[10];
   return ws_layout(*cfg, max_rows, off);
 }
 
@@ -578,7 +624,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
   if (!(s2 || xl2) || c.patch != 2 || c.in_ch != 4 || c.latent_hw % 32 || c.mlp_hidden != 4 * c.hidden ||
       c.freq_dim % 2 || c.freq_dim > 1024 || c.embed_dim < 1 || c.embed_dim > 64 || c.depth < 1)
     return SF_ERR_PARAMETER;
-  int64_t off[9];
+  int64_t off[10];
   if (ws_layout(c, max_rows, off) > ws_bytes) return SF_ERR_PARAMETER;
   auto* h = new sf_dit();
   h->cfg = c;
@@ -598,6 +644,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
   h->vt = (__nv_bfloat16*)(base + off[6]);
   h->attn = (__nv_bfloat16*)(base + off[7]);
   h->hmid = (__nv_bfloat16*)(base + off[8]);
+  h->h1 = (float*)(base + off[9]);
   const int64_t M = max_rows * h->tokens;
   const int64_t rows_pad = align_up(max_rows, 128);
   int rc = SF_OK;
