@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(256) cond_out_kernel(RowSrc src, int hidden, c
 }
 
 // ============================================================ K2+K4: patch embed + pos + LN1 modulate
-// One warp per token (grid-stride over tokens); lane owns columns
-// 128u + 4 lane + {0..3}.  Weights live in smem transposed ([PK][HID]) so a
-// warp's float4 reads are consecutive (conflict-free).
+// One warp per group of TOK consecutive tokens (grid-stride); lane owns columns
+// 128u + 4 lane + {0..3}.  Weights live in smem transposed ([PK][HID]); each
+// float4 weight read serves all TOK tokens of the group.
 template <int HID>
 __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
     const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
     float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
   constexpr int U = HID / 128;
   constexpr int PK = 16;  // C * P * P (4 * 2 * 2), checked at create
+  constexpr int TOK = HID <= 384 ? 4 : 2;
   extern __shared__ float swT[];  // [PK][HID]
   for (int idx = threadIdx.x; idx < HID * PK; idx += blockDim.x) {
     const int nn = idx / PK, k = idx % PK;  // pw is [HID][PK]
@@ -169,69 +170,99 @@ __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gw = HW / P, T = gw * gw;
+  const int64_t groups = total_tokens / TOK;  // T % TOK == 0: a group never straddles latents
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < total_tokens; tok += wstride) {
-    const int64_t ni = tok / T;
-    const int tau = (int)(tok % T);
-    const int pi = tau / gw, pj = tau % gw;
+  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
+    const int64_t tok0 = grp * TOK;
+    const int64_t ni = tok0 / T;
+    const int tau0 = (int)(tok0 % T);
     const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
-    float v[PK];
+    float v[TOK][PK];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int t = 0; t < TOK; ++t) {
+      const int pi = (tau0 + t) / gw, pj = (tau0 + t) % gw;
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const float2 t2 = *reinterpret_cast<const float2*>(xl + (int64_t)c * HW * HW + (pi * 2 + p) * HW + pj * 2);
-        v[(c * 2 + p) * 2 + 0] = t2.x;
-        v[(c * 2 + p) * 2 + 1] = t2.y;
-      }
-    float y[U][4];
-    float sum = 0.f;
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+        for (int p = 0; p < 2; ++p) {
+          const float2 t2 = *reinterpret_cast<const float2*>(xl + (int64_t)c * HW * HW + (pi * 2 + p) * HW + pj * 2);
+          v[t][(c * 2 + p) * 2 + 0] = t2.x;
+          v[t][(c * 2 + p) * 2 + 1] = t2.y;
+        }
+    }
+    // pass 1: residual y = patch . W + b + pos (bf16-rounded as stored) -> xres,
+    // row sums and sums of squares; pass 2 recomputes y (16 FMAs per element)
+    // for LayerNorm + modulate -> xmod.  Keeps the live set to one 128-column slice.
+    auto slice = [&](int u, float (&y)[TOK][4]) {
       const int n0 = 128 * u + 4 * lane;
       const float4 bb = *reinterpret_cast<const float4*>(pb + n0);
-      const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)tau * HID + n0);
-      float a0 = bb.x + pp.x, a1 = bb.y + pp.y, a2 = bb.z + pp.z, a3 = bb.w + pp.w;
-      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+      for (int t = 0; t < TOK; ++t) {
+        const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)(tau0 + t) * HID + n0);
+        y[t][0] = bb.x + pp.x;
+        y[t][1] = bb.y + pp.y;
+        y[t][2] = bb.z + pp.z;
+        y[t][3] = bb.w + pp.w;
+      }
 #pragma unroll
       for (int k = 0; k < PK; ++k) {
         const float4 wv = *reinterpret_cast<const float4*>(swT + k * HID + n0);
-        c0 += v[k] * wv.x;
-        c1 += v[k] * wv.y;
-        c2 += v[k] * wv.z;
-        c3 += v[k] * wv.w;
+#pragma unroll
+        for (int t = 0; t < TOK; ++t) {
+          y[t][0] += v[t][k] * wv.x;
+          y[t][1] += v[t][k] * wv.y;
+          y[t][2] += v[t][k] * wv.z;
+          y[t][3] += v[t][k] * wv.w;
+        }
       }
-      y[u][0] = __bfloat162float(__float2bfloat16_rn(c0 + a0));  // residual stored bf16
-      y[u][1] = __bfloat162float(__float2bfloat16_rn(c1 + a1));
-      y[u][2] = __bfloat162float(__float2bfloat16_rn(c2 + a2));
-      y[u][3] = __bfloat162float(__float2bfloat16_rn(c3 + a3));
-      sum += (y[u][0] + y[u][1]) + (y[u][2] + y[u][3]);
+#pragma unroll
+      for (int t = 0; t < TOK; ++t)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) y[t][r] = __bfloat162float(__float2bfloat16_rn(y[t][r]));  // stored bf16
+    };
+    float sum[TOK], sq[TOK];
+#pragma unroll
+    for (int t = 0; t < TOK; ++t) sum[t] = sq[t] = 0.f;
+#pragma unroll 1
+    for (int u = 0; u < U; ++u) {
+      float y[TOK][4];
+      slice(u, y);
+#pragma unroll
+      for (int t = 0; t < TOK; ++t) {
+        *reinterpret_cast<uint2*>(xres + (tok0 + t) * HID + 128 * u + 4 * lane) =
+            make_uint2(pack_bf16(y[t][0], y[t][1]), pack_bf16(y[t][2], y[t][3]));
+        sum[t] += (y[t][0] + y[t][1]) + (y[t][2] + y[t][3]);
+        sq[t] += (y[t][0] * y[t][0] + y[t][1] * y[t][1]) + (y[t][2] * y[t][2] + y[t][3] * y[t][3]);
+      }
     }
+    float mean[TOK], rstd[TOK];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mean = sum / HID;
-    float var = 0.f;
+    for (int t = 0; t < TOK; ++t) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-    const float rstd = rsqrtf(var / HID + ln_eps);
+      for (int o = 16; o; o >>= 1) {
+        sum[t] += __shfl_xor_sync(0xffffffffu, sum[t], o);
+        sq[t] += __shfl_xor_sync(0xffffffffu, sq[t], o);
+      }
+      mean[t] = sum[t] / HID;
+      rstd[t] = rsqrtf(fmaxf(sq[t] / HID - mean[t] * mean[t], 0.f) + ln_eps);
+    }
     const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
     const float* scale = shift + HID;
-#pragma unroll
+#pragma unroll 1
     for (int u = 0; u < U; ++u) {
+      float y[TOK][4];
+      slice(u, y);
       const int n0 = 128 * u + 4 * lane;
       const float4 sh = *reinterpret_cast<const float4*>(shift + n0);
       const float4 sc = *reinterpret_cast<const float4*>(scale + n0);
-      const float o0 = (y[u][0] - mean) * rstd * (1.0f + sc.x) + sh.x;
-      const float o1 = (y[u][1] - mean) * rstd * (1.0f + sc.y) + sh.y;
-      const float o2 = (y[u][2] - mean) * rstd * (1.0f + sc.z) + sh.z;
-      const float o3 = (y[u][3] - mean) * rstd * (1.0f + sc.w) + sh.w;
-      *reinterpret_cast<uint2*>(xres + tok * HID + n0) =
-          make_uint2(pack_bf16(y[u][0], y[u][1]), pack_bf16(y[u][2], y[u][3]));
-      *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+#pragma unroll
+      for (int t = 0; t < TOK; ++t) {
+        const float o0 = (y[t][0] - mean[t]) * rstd[t] * (1.0f + sc.x) + sh.x;
+        const float o1 = (y[t][1] - mean[t]) * rstd[t] * (1.0f + sc.y) + sh.y;
+        const float o2 = (y[t][2] - mean[t]) * rstd[t] * (1.0f + sc.z) + sh.z;
+        const float o3 = (y[t][3] - mean[t]) * rstd[t] * (1.0f + sc.w) + sh.w;
+        *reinterpret_cast<uint2*>(xmod + (tok0 + t) * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      }
     }
   }
 }
@@ -303,8 +334,24 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
-// One warp per token (grid-stride).  16 output features per token: lane f < 16
-// ends up owning feature f = (p*2 + q)*4 + c, i.e. one latent pixel.
+// One warp per group of 4 consecutive tokens (grid-stride).  Lane partial dot
+// products over its 4 x U columns for all 4 tokens x 16 output features (each
+// float4 weight read serves the 4 tokens), then a butterfly reduce-scatter
+// (31 shuffles of 64 -> 2 values per lane): lane ends up owning token lane/8,
+// features 2 (lane%8) and 2 (lane%8) + 1, i.e. two latent pixels.
+// One reduce-scatter round: lanes with bit `o` keep the upper half of the live
+// 2H values, the others the lower half; each adds its partner's copy.
+template <int H, int N>
+__device__ __forceinline__ void bfly_round(float (&a)[N], int o, int lane) {
+  const bool hi = (lane & o) != 0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const float send = hi ? a[i] : a[i + H];
+    const float keep = hi ? a[i + H] : a[i];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+}
+
 template <int HID, bool STREAM>
 __global__ void __launch_bounds__(256) final_layer_kernel(
     const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
@@ -318,6 +365,7 @@ __global__ void __launch_bounds__(256) final_layer_kernel(
     int64_t* __restrict__ frame_ids, int64_t total_tokens) {
   constexpr int U = HID / 128;
   constexpr int PK = 16;
+  constexpr int TOK = 4;
   extern __shared__ float sw[];  // [PK][HID] + bias[PK]
   for (int idx = threadIdx.x; idx < PK * HID; idx += blockDim.x) sw[idx] = __bfloat162float(fw[idx]);
   for (int idx = threadIdx.x; idx < PK; idx += blockDim.x) sw[PK * HID + idx] = fb[idx];
@@ -328,79 +376,94 @@ __global__ void __launch_bounds__(256) final_layer_kernel(
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
   int64_t j = 0;
   if constexpr (STREAM) j = ctl[1];
+  const int my_t = lane >> 3, my_f = 2 * (lane & 7);  // after the reduce-scatter
 
-  auto project = [&](int64_t net_row, int tau) -> float {
-    const __nv_bfloat16* xr = xmod + (net_row * T + tau) * HID;
-    float xv[U][4];
+  // eps (pre-CFG) of features my_f, my_f+1 of token tau0 + my_t of network row net_row
+  auto project = [&](int64_t net_row, int tau0) -> float2 {
+    float a[TOK * PK];
 #pragma unroll
+    for (int i = 0; i < TOK * PK; ++i) a[i] = 0.f;
+#pragma unroll 1
     for (int u = 0; u < U; ++u) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(xr + 128 * u + 4 * lane);
-      const float2 a = unpack_bf16(raw.x), b = unpack_bf16(raw.y);
-      xv[u][0] = a.x;
-      xv[u][1] = a.y;
-      xv[u][2] = b.x;
-      xv[u][3] = b.y;
-    }
-    float mine = 0.f;
+      float xv[TOK][4];
 #pragma unroll
-    for (int f = 0; f < PK; ++f) {
-      float acc = 0.f;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float4 wv = *reinterpret_cast<const float4*>(sw + f * HID + 128 * u + 4 * lane);
-        acc += xv[u][0] * wv.x + xv[u][1] * wv.y + xv[u][2] * wv.z + xv[u][3] * wv.w;
+      for (int t = 0; t < TOK; ++t) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(xmod + (net_row * T + tau0 + t) * HID + 128 * u + 4 * lane);
+        const float2 p0 = unpack_bf16(raw.x), p1 = unpack_bf16(raw.y);
+        xv[t][0] = p0.x;
+        xv[t][1] = p0.y;
+        xv[t][2] = p1.x;
+        xv[t][3] = p1.y;
       }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == f) mine = acc;
+      for (int f = 0; f < PK; ++f) {
+        const float4 wv = *reinterpret_cast<const float4*>(sw + f * HID + 128 * u + 4 * lane);
+#pragma unroll
+        for (int t = 0; t < TOK; ++t)
+          a[t * PK + f] += xv[t][0] * wv.x + xv[t][1] * wv.y + xv[t][2] * wv.z + xv[t][3] * wv.w;
+      }
     }
-    return mine + (lane < PK ? sw[PK * HID + lane] : 0.f);
+    // butterfly reduce-scatter over the 64 (token, feature) partials
+    bfly_round<32>(a, 16, lane);
+    bfly_round<16>(a, 8, lane);
+    bfly_round<8>(a, 4, lane);
+    bfly_round<4>(a, 2, lane);
+    bfly_round<2>(a, 1, lane);
+    return make_float2(a[0] + sw[PK * HID + my_f], a[1] + sw[PK * HID + my_f + 1]);
   };
 
-  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < total_tokens; tok += wstride) {
-    const int64_t lr = tok / T;
-    const int tau = (int)(tok % T);
-    float e = project(STREAM && cfg ? lr + lat_rows : lr, tau);
+  const int64_t groups = total_tokens / TOK;
+  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
+    const int64_t tok0 = grp * TOK;
+    const int64_t lr = tok0 / T;
+    const int tau0 = (int)(tok0 % T);
+    float2 e2 = project(STREAM && cfg ? lr + lat_rows : lr, tau0);
     if constexpr (STREAM) {
       if (cfg) {
-        const float eu = project(lr, tau);
-        e = __fadd_rn(eu, __fmul_rn(w, __fsub_rn(e, eu)));  // handle_cfg (models.py:288-293)
+        const float2 eu = project(lr, tau0);
+        e2.x = __fadd_rn(eu.x, __fmul_rn(w, __fsub_rn(e2.x, eu.x)));  // handle_cfg (models.py:288-293)
+        e2.y = __fadd_rn(eu.y, __fmul_rn(w, __fsub_rn(e2.y, eu.y)));
       }
     }
-    if (lane >= PK) continue;
-    // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
-    const int c = lane % C, q = (lane / C) % P, p = lane / (C * P);
+    const int tau = tau0 + my_t;
     const int pi = tau / gw, pj = tau % gw;
-    const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
-    if constexpr (!STREAM) {
-      eps_out[lr * D + idx] = e;
-    } else {
-      const int64_t stage = row_info[lr * 4 + 0];
-      const int64_t g = row_info[lr * 4 + 1];
-      const bool active = row_info[lr * 4 + 2] != 0;
-      const int64_t s = row_info[lr * 4 + 3];
-      const int64_t k = lr % n;
-      const bool refill_slot = (k == (j + 1) % n);
-      const bool admit = refill_slot && (j + 1 < m);
-      const bool retiring = active && (stage + 1 == n);
-      if (refill_slot && tau == 0 && lane == 0) frame_ids[s] = retiring ? g : -1;
-      float* xr = x_ring + lr * D;
-      const float noise =
-          admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
-      if (active) {
-        const double* pp = stage_params + stage * SF_PARAM_STRIDE;
-        const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
-        const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
-        const bool at_end = pp[SF_P_AT_END] != 0.0;
-        const float xo = xr[idx];
-        // velocity.py:125-130 in fp32
-        const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
-        const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
-        const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
-        if (retiring) frames_out[s * D + idx] = xn;
-        xr[idx] = admit ? noise : xn;
-      } else if (admit) {
-        xr[idx] = noise;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int f = my_f + h;
+      const float e = h ? e2.y : e2.x;
+      // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
+      const int c = f % C, q = (f / C) % P, p = f / (C * P);
+      const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
+      if constexpr (!STREAM) {
+        eps_out[lr * D + idx] = e;
+      } else {
+        const int64_t stage = row_info[lr * 4 + 0];
+        const int64_t g = row_info[lr * 4 + 1];
+        const bool active = row_info[lr * 4 + 2] != 0;
+        const int64_t s = row_info[lr * 4 + 3];
+        const int64_t k = lr % n;
+        const bool refill_slot = (k == (j + 1) % n);
+        const bool admit = refill_slot && (j + 1 < m);
+        const bool retiring = active && (stage + 1 == n);
+        if (refill_slot && tau == 0 && f == 0) frame_ids[s] = retiring ? g : -1;
+        float* xr = x_ring + lr * D;
+        const float noise =
+            admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
+        if (active) {
+          const double* pp = stage_params + stage * SF_PARAM_STRIDE;
+          const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
+          const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
+          const bool at_end = pp[SF_P_AT_END] != 0.0;
+          const float xo = xr[idx];
+          // velocity.py:125-130 in fp32
+          const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
+          const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
+          const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
+          if (retiring) frames_out[s * D + idx] = xn;
+          xr[idx] = admit ? noise : xn;
+        } else if (admit) {
+          xr[idx] = noise;
+        }
       }
     }
   }
@@ -595,7 +658,7 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   const sf_dit_config& c = h->cfg;
   const int64_t tokens = rows * h->tokens;
   const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8);
   auto kern = c.hidden == 384 ? patch_embed_ln_kernel<384> : patch_embed_ln_kernel<1152>;
   kern<<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
                                 h->w.patch_b, h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens);
@@ -719,7 +782,7 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = rows * h->tokens;
   auto fk = c.hidden == 384 ? final_layer_kernel<384, false> : final_layer_kernel<1152, false>;
-  fk<<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
+  fk<<<(unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, rows, eps_out,
       nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr, tokens);
   return cuda_status();
@@ -743,7 +806,7 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = R * h->tokens;
   auto fk = c.hidden == 384 ? final_layer_kernel<384, true> : final_layer_kernel<1152, true>;
-  fk<<<(unsigned)std::min<int64_t>((tokens + 7) / 8, 148 * 8), 256, final_smem(c), st>>>(
+  fk<<<(unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8), 256, final_smem(c), st>>>(
       h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
       m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
   mark(h, P_FINAL, st);
