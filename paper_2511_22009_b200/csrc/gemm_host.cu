@@ -173,3 +173,9 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
 }
 
 }  // namespace sf
+
+#if SF_GEMM_TRACE
+extern "C" int sf_gemm_trace_read(long long* dst) {
+  return cudaMemcpyFromSymbol(dst, sf::g_gemm_trace, sizeof(long long) * 8 * 64) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -20,6 +20,21 @@
 
 namespace sf {
 
+#ifndef SF_GEMM_TRACE
+#define SF_GEMM_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_gemm_trace_read)
+#endif
+#if SF_GEMM_TRACE
+__device__ long long g_gemm_trace[8 * 64];
+#define GTR(role, idx)                                                               \
+  do {                                                                               \
+    if (blockIdx.x == 0 && (idx) < 64) g_gemm_trace[(role) * 64 + (idx)] = clock64(); \
+  } while (0)
+#else
+#define GTR(role, idx) \
+  do {                 \
+  } while (0)
+#endif
+
 enum EpiKind : int {
   EPI_F32 = 0,     // out f32 [M, ldo]  = acc + bias
   EPI_BF16 = 1,    // out bf16 [M, ldo] = acc + bias
@@ -221,6 +236,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
+      if (lane == 0) GTR(0, local);
       const uint32_t d = tmem_base + acc * C::ACC_STRIDE;
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
@@ -241,6 +257,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
         }
         __syncwarp();
       }
+      if (lane == 0) GTR(1, local);
     }
   } else {
     // ---------------- epilogue warps
@@ -309,8 +326,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
         __syncwarp();
       }
       named_bar_sync(5, EPI_THREADS);  // vectors staged
+      if (warp == 2 && lane == 0) GTR(2, local);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (warp == 2 && lane == 0) GTR(3, local);
       if (ep.no_store == 2) {  // diagnostics: main loop only
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -617,6 +636,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
         ring += 2 * NQ;
       }
     }
+    if (warp == 2 && lane == 0) GTR(5, 0);
     if (lane == 0) bulk_wait<0>();  // all output stores of this warp have landed
     __syncwarp();
   }
