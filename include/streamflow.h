@@ -105,6 +105,12 @@ int sf_mock_keys(int64_t model_seed, const int64_t* ids, const double* ts, const
                  int32_t E, uint64_t* keys, void* stream);
 int sf_mock_eps(const uint64_t* keys, int64_t B, int64_t D, double* out, void* stream);
 
+/* K13 -- AnalyticLinearModel._compute (models.py:176-185): eps_i = A x_i + t_i b in fp64,
+ * row by row (batch-decomposition invariant).  A [D, D] and b [D] fp64, x [B, D] in
+ * x_dtype (SF_F64 / SF_F32), ts [B] fp64 -> out [B, D] fp64. */
+int sf_analytic_eps(const double* A, const double* b, const void* x, int x_dtype, const double* ts, int64_t B,
+                    int64_t D, double* out, void* stream);
+
 /* ---- device-resident stream batch (pipeline.py:139-220) ----
  * S independent streams x n in-flight slots.  Ring row r = s*n + k holds the
  * generation g of stream s with g = k (mod n); at iteration j its stage is

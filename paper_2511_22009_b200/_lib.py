@@ -55,6 +55,7 @@ SIGNATURES = {
     "sf_gemm_qkv_hd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, C.c_float, _vp],
     "sf_gemm_res": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _vp],
     "sf_ln_modulate": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, C.c_float, _vp],
+    "sf_analytic_eps": [_vp, _vp, _vp, C.c_int, _vp, _i64, _i64, _vp, _vp],
     "sf_attention": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
     "sf_attention_hd": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp],
 }

@@ -331,6 +331,28 @@ static inline int grid_for(int64_t n, int threads) {
 
 using namespace sf;
 
+namespace sf {
+// ---------------------------------------------------------------- K13: analytic linear model
+// eps_i = A x_i + t_i b (models.py:176-185), fp64, row by row: output (i, j) is a
+// sequential fp64 dot product over k, so a row's result never depends on the
+// batch it was submitted in (dispatcher bit-identity, models.py:142-146).
+template <typename XT>
+__global__ void analytic_eps_kernel(const double* __restrict__ A, const double* __restrict__ bvec,
+                                    const XT* __restrict__ x, const double* __restrict__ ts, int64_t D,
+                                    double* __restrict__ out) {
+  const int64_t i = blockIdx.y;
+  const XT* xi = x + i * D;
+  const double ti = ts[i];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < D; j += (int64_t)gridDim.x * blockDim.x) {
+    const double* aj = A + j * D;
+    double acc = 0.0;
+    for (int64_t k = 0; k < D; ++k) acc = __dadd_rn(acc, __dmul_rn(aj[k], (double)xi[k]));
+    out[i * D + j] = __dadd_rn(acc, __dmul_rn(ti, bvec[j]));
+  }
+}
+
+}  // namespace sf
+
 extern "C" {
 
 int sf_window_params(const sf_schedule* sched, const double* ts, int64_t B, double* out, uint32_t* status,
@@ -383,6 +405,19 @@ int sf_mock_keys(int64_t model_seed, const int64_t* ids, const double* ts, const
   if (B < 0 || E < 1 || E > 64) return SF_ERR_PARAMETER;
   if (B == 0) return SF_OK;
   mock_keys_kernel<<<grid_for(B, 64), 64, 0, (cudaStream_t)stream>>>(model_seed, ids, ts, row_embs, B, E, keys);
+  return cuda_status();
+}
+
+int sf_analytic_eps(const double* A, const double* b, const void* x, int x_dtype, const double* ts, int64_t B,
+                    int64_t D, double* out, void* stream) {
+  if (B < 0 || D < 1 || B > 65535 || (x_dtype != SF_F64 && x_dtype != SF_F32)) return SF_ERR_PARAMETER;
+  if (B == 0) return SF_OK;
+  dim3 grid(grid_for(D, 128) > 64 ? 64 : grid_for(D, 128), (unsigned)B);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (x_dtype == SF_F64)
+    sf::analytic_eps_kernel<double><<<grid, 128, 0, st>>>(A, b, (const double*)x, ts, D, out);
+  else
+    sf::analytic_eps_kernel<float><<<grid, 128, 0, st>>>(A, b, (const float*)x, ts, D, out);
   return cuda_status();
 }
 

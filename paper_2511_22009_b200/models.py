@@ -148,6 +148,49 @@ class SeededMockModel(VelocityModel):
         return ModelOutput(epsilon=eps_o, aux=None if aux is None else [_host_if(batch.data, a) for a in aux])
 
 
+class AnalyticLinearModel(VelocityModel):
+    """Closed-form model eps_i = A x_i + t_i b (models.py:139-185) on the GPU (kernel
+    K13): fp64, one output element per thread as a sequential dot product, so a row's
+    result does not depend on the batch it arrives in (models.py:142-146).  Defaults
+    A = 0.1 I, b = 0.05 (models.py:162-165); conditioning does not enter the map."""
+
+    def __init__(self, dim: int = 16, embed_dim: int = 8, cost_us: float = 0.0, a_matrix=None, b_vector=None,
+                 aux_scales: tuple = ()):
+        super().__init__(dim=dim, embed_dim=embed_dim, cost_us=cost_us)
+        a_matrix = 0.1 * np.eye(dim) if a_matrix is None else a_matrix
+        b_vector = 0.05 * np.ones(dim) if b_vector is None else b_vector
+        self.a_matrix = np.asarray(a_matrix, dtype=np.float64)
+        self.b_vector = np.asarray(b_vector, dtype=np.float64)
+        if self.a_matrix.shape != (dim, dim):
+            raise ParameterError(f"a_matrix shape {self.a_matrix.shape} != ({dim}, {dim})")
+        if self.b_vector.shape != (dim,):
+            raise ParameterError(f"b_vector shape {self.b_vector.shape} != ({dim},)")
+        self.aux_scales = aux_scales
+        self._a_dev = None
+
+    def _device_ab(self):
+        if self._a_dev is None:
+            self._a_dev = (torch.from_numpy(self.a_matrix).cuda(), torch.from_numpy(self.b_vector).cuda())
+        return self._a_dev
+
+    def _compute(self, batch: LatentBatch, cond: Conditioning) -> ModelOutput:
+        a_dev, b_dev = self._device_ab()
+        if _is_torch(batch.data):
+            xdt = torch.float32 if batch.data.dtype == torch.float32 else torch.float64
+        else:
+            xdt = torch.float32 if np.asarray(batch.data).dtype == np.float32 else torch.float64
+        x = _to_device(batch.data, xdt).contiguous()
+        ts = _to_device(batch.timesteps, torch.float64)
+        B = x.shape[0]
+        out = torch.empty(B, self.dim, dtype=torch.float64, device=x.device)
+        _lib.call("sf_analytic_eps", a_dev.data_ptr(), b_dev.data_ptr(), x.data_ptr(),
+                  _lib.SF_F32 if xdt == torch.float32 else _lib.SF_F64, ts.data_ptr(), B, self.dim, out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        aux = [scale * out for scale in self.aux_scales] if self.aux_scales else None
+        return ModelOutput(epsilon=_host_if(batch.data, out),
+                           aux=None if aux is None else [_host_if(batch.data, a) for a in aux])
+
+
 class DiTVelocityModel(VelocityModel):
     """DiT velocity field (dit.py) as a VelocityModel plugin.  ``forward`` runs
     the native sf_dit_forward; StreamBatch uses the fused sf_dit_stream_step."""
