@@ -24,6 +24,7 @@ import torch
 
 from . import _lib
 from .errors import ParameterError, StateError
+from .engine import model_forward
 from .models import (Conditioning, DiTVelocityModel, SeededMockModel, VelocityModel, apply_cfg, busy_wait_us,
                      handle_cfg)
 from .schedule import DeviceSchedule, TimeWindowSchedule
@@ -287,9 +288,9 @@ class StreamBatch:
                             ids=ids[s * per:(s + 1) * per])
             if c.guidance_scale != 1.0:
                 d2, c2 = apply_cfg(b, c)
-                out = handle_cfg(self.model.forward(d2, c2), c.guidance_scale)
+                out = handle_cfg(model_forward(self.model, d2, c2), c.guidance_scale)
             else:
-                out = self.model.forward(b, c)
+                out = model_forward(self.model, b, c)
             e = out.epsilon if isinstance(out.epsilon, torch.Tensor) else torch.from_numpy(out.epsilon).cuda()
             eps_rows.append(e.to(self.x_ring.dtype) if e.dtype not in (torch.float32, torch.float64) else e)
         eps = torch.cat(eps_rows)
@@ -414,9 +415,9 @@ def run_vanilla(m: int, n: int, model: VelocityModel, cond: Conditioning, seed: 
             batch = LatentBatch(data=latent[None, :], timesteps=np.asarray([t]), ids=np.asarray([g], dtype=np.int64))
             if cond.guidance_scale != 1.0:
                 d2, c2 = apply_cfg(batch, cond)
-                eps = handle_cfg(model.forward(d2, c2), cond.guidance_scale).epsilon
+                eps = handle_cfg(model_forward(model, d2, c2), cond.guidance_scale).epsilon
             else:
-                eps = model.forward(batch, cond).epsilon
+                eps = model_forward(model, batch, cond).epsilon
             stats.model_calls += 1
             busy_wait_us(sched_cost_us)
             latent, t = sequential_velocity_step(np.asarray(eps)[0], latent, t, sched, stats.step_stats)
