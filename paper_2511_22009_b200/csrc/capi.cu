@@ -80,7 +80,8 @@ int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float
                             tokens_per_slot, ln_eps, (cudaStream_t)stream);
 }
 
-// Diagnostics only (not in the header): 1 = skip epilogue stores, 2 = main loop only.
+// Diagnostics only (not in the header): 1 = skip epilogue stores, 2 = main loop only,
+// 3 / 4 = force the single-CTA 384-wide / the 2-CTA cluster RES_LN kernel.
 static int g_diag_res_ln = 0;
 int sf_diag_res_ln(int mode) {
   g_diag_res_ln = mode;
@@ -91,8 +92,11 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream) {
   if (N != 384 || K % 64 || M < 1 || M % tokens_per_slot || tokens_per_slot % 128) return SF_ERR_PARAMETER;
+  // 2-CTA cluster kernel (192-column slices, statistics exchanged through DSMEM) unless
+  // diagnostics ask for the single-CTA 384-wide tile (mode 3)
+  const bool cl = g_diag_res_ln == 4 || (g_diag_res_ln != 3 && K >= 1024);  // as the DiT runtime: cluster for long K
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, 384) != SF_OK) return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, cl ? 192 : 384) != SF_OK) return SF_ERR_CUDA;
   if (make_out_map32(&maps.d[0], xres, M, N) != SF_OK || make_out_map32(&maps.d[1], xmod, M, N) != SF_OK)
     return SF_ERR_CUDA;
   EpiParams ep{};
@@ -105,8 +109,9 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
   ep.ln_eps = ln_eps;
   ep.tokens_per_slot = tokens_per_slot;
   ep.M = (int)M;
-  ep.no_store = g_diag_res_ln;
-  return launch_gemm(EPI_RES_LN, 384, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  ep.no_store = g_diag_res_ln >= 3 ? 0 : g_diag_res_ln;
+  return cl ? launch_gemm(EPI_RES_LN2, 192, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream)
+            : launch_gemm(EPI_RES_LN, 384, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -626,7 +626,14 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if (fused_ln) {
-        if ((rc = launch_gemm(EPI_RES_LN, 384, gm, (int)M, H, K, ep, st))) return rc;
+        // fc2 (K = 1536): 2-CTA cluster kernel (192-column slices, double-buffered
+        // accumulators, LayerNorm statistics through DSMEM); proj (K = 384): one CTA
+        // per 384-wide row tile (its short main loop does not amortise the exchange)
+        if (half == 1) {
+          if ((rc = launch_gemm(EPI_RES_LN2, 192, gm, (int)M, H, K, ep, st))) return rc;
+        } else {
+          if ((rc = launch_gemm(EPI_RES_LN, 384, gm, (int)M, H, K, ep, st))) return rc;
+        }
         mark(h, cls, st);
       } else {
         if ((rc = launch_gemm(EPI_RES, 128, gm, (int)M, H, K, ep, st))) return rc;
@@ -730,7 +737,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
       rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
       rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);
       rc |= make_out_map32(&h->g_proj[l].d[1], h->xmod, M, H);
-      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 384);
+      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 192);
       rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
       rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
     } else {  // RES epilogue (128-wide tiles) + LayerNorm pass

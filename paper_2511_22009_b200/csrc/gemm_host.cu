@@ -86,7 +86,7 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
 
 template <int BN, int KIND>
 constexpr int epi_warps() {
-  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;  // EPI_RES: 8
+  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;  // EPI_RES, EPI_RES_LN2: 8
 }
 
 template <int BN, int KIND>
@@ -95,9 +95,9 @@ static int set_attr() {
   if (!done) {
     constexpr int W = epi_warps<BN, KIND>();
     const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, W>::SMEM_BYTES);
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, W, KIND>::SMEM_BYTES);
     if (err != cudaSuccess) {
-      fprintf(stderr, "streamflow: gemm<%d,%d> smem attribute (%d B) failed: %s\n", BN, KIND, GemmCfg<BN, W>::SMEM_BYTES,
+      fprintf(stderr, "streamflow: gemm<%d,%d> smem attribute (%d B) failed: %s\n", BN, KIND, GemmCfg<BN, W, KIND>::SMEM_BYTES,
               cudaGetErrorString(err));
       return SF_ERR_CUDA;
     }
@@ -119,6 +119,7 @@ int prepare_gemm_kernels() {
   rc |= set_attr<384, EPI_RES_LN>();
   rc |= set_attr<144, EPI_QKV>();
   rc |= set_attr<128, EPI_RES>();
+  rc |= set_attr<192, EPI_RES_LN2>();
   return rc;
 }
 
@@ -136,15 +137,35 @@ static int sm_count() {
 template <int BN, int KIND>
 static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams& ep, cudaStream_t st) {
   constexpr int W = epi_warps<BN, KIND>();
-  using C = GemmCfg<BN, W>;
+  using C = GemmCfg<BN, W, KIND>;
   if (K % C::BK) return SF_ERR_PARAMETER;
   if (set_attr<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
   const int tiles = (N / BN) * ((M + C::BM - 1) / C::BM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   EpiParams e = ep;
   e.M = M;
-  gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(maps, N, K, e);
-  const cudaError_t err = cudaGetLastError();
+  cudaError_t err;
+  if constexpr (KIND == EPI_RES_LN2) {
+    // one cluster of XCH_CL CTAs per row tile in flight: grid = whole clusters
+    cudaLaunchConfig_t cfg = {};
+    const int rows = (M + C::BM - 1) / C::BM, max_cl = sm_count() / XCH_CL;
+    cfg.gridDim = dim3((unsigned)(XCH_CL * (rows < max_cl ? rows : max_cl)));
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = XCH_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W>, maps, N, K, e);
+    if (err == cudaSuccess) err = cudaGetLastError();
+  } else {
+    gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(maps, N, K, e);
+    err = cudaGetLastError();
+  }
   if (err != cudaSuccess) {
     fprintf(stderr, "streamflow: gemm<%d,%d> launch failed: %s (smem %d, threads %d)\n", BN, KIND,
             cudaGetErrorString(err), C::SMEM_BYTES, C::THREADS);
@@ -168,6 +189,7 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
   SF_CASE(384, EPI_RES_LN)
   SF_CASE(144, EPI_QKV)
   SF_CASE(128, EPI_RES)
+  SF_CASE(192, EPI_RES_LN2)
 #undef SF_CASE
   return SF_ERR_PARAMETER;
 }

@@ -42,7 +42,10 @@ enum EpiKind : int {
   EPI_QKV = 3,     // scatter to Q,K [rows, H, T, 64] bf16 and V^T [rows, H, 64, T] fp16; Q pre-scaled
   EPI_RES_LN = 4,  // x += gate*(acc+bias) (bf16 residual); xmod = LN(x)*(1+scale)+shift
   EPI_RES = 5,     // x += gate*(acc+bias) only (wide rows; LayerNorm runs as its own pass)
+  EPI_RES_LN2 = 6, // RES_LN over a cluster of N/BN CTAs (BN = 192): each CTA owns a column slice of
+                   // the same 128 rows, LayerNorm row statistics meet in distributed shared memory
 };
+constexpr int XCH_CL = 2;  // RES_LN2 cluster size (384-wide rows / 192-column tiles)
 
 struct EpiParams {
   const float* bias;  // [N]
@@ -73,7 +76,7 @@ struct GemmMaps {
   CUtensorMap a, b, d[3];
 };
 
-template <int BN, int EPI_WARPS>
+template <int BN, int EPI_WARPS, int KIND>
 struct GemmCfg {
   static constexpr int BM = 128;
   static constexpr int BK = BN > 256 ? 32 : 64;  // K elements per stage (64 B / 128 B rows)
@@ -94,11 +97,14 @@ struct GemmCfg {
   // (RES_LN: a 3-deep ring per warp; residual chunks are TMA-loaded into it and
   // overwritten in place by the updated residual before its TMA store)
   // (head dim 72 QKV, BN = 144: 32 x 144 B Q/K rows or 72 x 64 B V^T rows per buffer)
-  static constexpr int OUT_BUF = BN == 144 ? 5120 : EPI_WARPS == 12 ? 2048 : 4096;
-  static constexpr int OUT_NBUF = EPI_WARPS == 12 ? 3 : 2;
+  static constexpr bool LN_RING = KIND == EPI_RES_LN || KIND == EPI_RES_LN2;  // 32-column SW64 chunks
+  static constexpr int OUT_BUF = BN == 144 ? 5120 : LN_RING ? 2048 : 4096;
+  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : 2;  // RES_LN(2): one buffer per chunk
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
-  static constexpr int RBAR_BYTES = EPI_WARPS * 3 * 8;  // residual-chunk barriers (RES_LN ring)
-  static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES + RBAR_BYTES;
+  static constexpr int RBAR_BYTES = EPI_WARPS * 4 * 8;  // residual-chunk barriers (one per staging buffer)
+  // RES_LN2 exchange: [tile parity][pass][source CTA][column group][128 rows] floats
+  static constexpr int XCH_BYTES = KIND == EPI_RES_LN2 ? 2 * 2 * XCH_CL * 2 * 128 * 4 : 0;
+  static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES + RBAR_BYTES + XCH_BYTES;
   static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int SMEM_BYTES = FIXED + STAGES * STAGE_BYTES;
@@ -159,9 +165,9 @@ struct OutStageT {
 };
 
 template <int BN, int KIND, int EPI_WARPS>
-__global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
+__global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ GemmMaps maps, int N, int K, EpiParams ep) {
-  using C = GemmCfg<BN, EPI_WARPS>;
+  using C = GemmCfg<BN, EPI_WARPS, KIND>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array (keeps the pointer in the shared window: LDS/STS, not generic)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -177,6 +183,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
   uint64_t* tempty = tfull + C::ACC_STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + C::ACC_STAGES);
   uint64_t* rbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [EPI_WARPS][3]
+  float* xch = reinterpret_cast<float*>(rbar + EPI_WARPS * 4);  // RES_LN2 exchange
+  uint64_t* xbar = tempty + C::ACC_STAGES + 1;                   // RES_LN2: [parity][pass], one arrive per CTA
+  constexpr bool CLUSTER = KIND == EPI_RES_LN2;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -184,6 +193,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
   const int num_m = (ep.M + C::BM - 1) / C::BM;
   const int total = num_m * num_n;
   const int num_kb = K / C::BK;
+  // Tile sequence: default = all (m, n) tiles N-fastest over the grid; cluster mode =
+  // the cluster walks row tiles m, CTA rank r of the cluster owns column slice n = r.
+  const uint32_t crank = CLUSTER ? cluster_ctarank() : 0u;
+  const int t_first = CLUSTER ? (int)(blockIdx.x / XCH_CL) : (int)blockIdx.x;
+  const int t_stride = CLUSTER ? (int)(gridDim.x / XCH_CL) : (int)gridDim.x;
+  const int t_limit = CLUSTER ? num_m : total;
+  auto tile_m0 = [&](int tile) { return CLUSTER ? tile * C::BM : (tile / num_n) * C::BM; };
+  auto tile_n0 = [&](int tile) { return CLUSTER ? (int)crank * BN : (tile % num_n) * BN; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a);
@@ -196,11 +213,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS * 32);
     }
-    if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES)
-      for (int i = 0; i < EPI_WARPS * 3; ++i) mbar_init(&rbar[i], 1);
+    if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES || KIND == EPI_RES_LN2)
+      for (int i = 0; i < EPI_WARPS * 4; ++i) mbar_init(&rbar[i], 1);
+    if constexpr (CLUSTER)
+      for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], XCH_CL * EPI_WARPS * 32);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if constexpr (CLUSTER) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -210,8 +230,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     if (lane == 0) {
       // ---------------- TMA producer (ring continues across tiles)
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * C::BM, n0 = (tile % num_n) * BN;
+      for (int tile = t_first; tile < t_limit; tile += t_stride) {
+        const int m0 = tile_m0(tile), n0 = tile_n0(tile);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -232,7 +252,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     const uint64_t a_desc0 = kmajor_desc<C::SWZ>(smem_u32(sA));
     const uint64_t b_desc0 = kmajor_desc<C::SWZ>(smem_u32(sB));
     uint32_t it = 0, local = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
+    for (int tile = t_first; tile < t_limit; tile += t_stride, ++local) {
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
@@ -269,11 +289,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
     const int et = threadIdx.x - 64;
     using OutStage = OutStageT<C::OUT_BUF>;
     OutStage out{sOut + e * C::OUT_NBUF * C::OUT_BUF, 0};
-    uint32_t ring = 0, rpar = 0;  // RES_LN: ring uses so far, per-buffer load parity bits
+    uint32_t ring = 0;  // RES: per-buffer load parity bits
     const bool do_store = !ep.no_store;
     uint32_t local = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++local) {
-      const int m0 = (tile / num_n) * C::BM, n0 = (tile % num_n) * BN;
+    for (int tile = t_first; tile < t_limit; tile += t_stride, ++local) {
+      const int m0 = tile_m0(tile), n0 = tile_n0(tile);
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       const int r0 = m0 + quarter * 32;  // first row of this warp
       const int row = r0 + lane;
@@ -287,27 +307,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
       for (int c = et; c < BN; c += EPI_THREADS) {
         vb[c] = ep.bias[n0 + c];
         if constexpr (KIND == EPI_RES) vb[BN + c] = ep.gate[(int64_t)slot * ep.vec_stride + n0 + c];
-        if constexpr (KIND == EPI_RES_LN) {
+        if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
           const int64_t o = (int64_t)slot * ep.vec_stride + n0 + c;
           vb[BN + c] = ep.gate[o];
           vb[2 * BN + c] = ep.shift[o];
           vb[3 * BN + c] = ep.scale[o];
         }
       }
-      // RES_LN: residual chunks (32 rows x 32 columns) are TMA-loaded into this
-      // warp's staging ring; the first two are issued before the accumulator wait
-      // so their latency hides under the main loop.
+      // RES_LN / RES_LN2: all residual chunks (32 rows x 32 columns) of this thread's
+      // columns are TMA-loaded into the warp's staging buffers (chunk q -> buffer q)
+      // before the accumulator wait, so their latency hides under the main loop;
+      // pass 1 overwrites them in place with the updated residual (then stored),
+      // pass 3 with the modulated LayerNorm output.
       uint8_t* const rbuf0 = sOut + e * C::OUT_NBUF * C::OUT_BUF;
-      auto res_load = [&](uint32_t use, int q) {  // lane 0: residual chunk q into the buffer of ring use `use`
-        const uint32_t b = use % 3;
-        mbar_expect_tx(&rbar[e * 3 + b], C::OUT_BUF);
-        tma_load_2d(rbuf0 + b * C::OUT_BUF, &maps.d[0], &rbar[e * 3 + b], n0 + c_lo + 32 * q, r0);
-      };
-      if constexpr (KIND == EPI_RES_LN) {
+      if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
         if (lane == 0) {
-          bulk_wait_read<1>();  // the previous users of these two buffers (stores) have read them
-          res_load(ring, 0);
-          res_load(ring + 1, 1);
+          bulk_wait_read<0>();  // the previous tile's stores have read every buffer
+#pragma unroll
+          for (int q = 0; q < COLS / 32; ++q) {
+            mbar_expect_tx(&rbar[e * 4 + q], C::OUT_BUF);
+            tma_load_2d(rbuf0 + q * C::OUT_BUF, &maps.d[0], &rbar[e * 4 + q], n0 + c_lo + 32 * q, r0);
+          }
         }
         __syncwarp();
       }
@@ -319,8 +339,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           bulk_wait_read<0>();  // previous tile's stores have read both buffers
 #pragma unroll
           for (int c = 0; c < COLS / 64; ++c) {
-            mbar_expect_tx(&rbar[e * 3 + c], 4096);
-            tma_load_2d(rbuf0 + c * 4096, &maps.d[0], &rbar[e * 3 + c], n0 + c_lo + 64 * c, r0);
+            mbar_expect_tx(&rbar[e * 4 + c], 4096);
+            tma_load_2d(rbuf0 + c * 4096, &maps.d[0], &rbar[e * 4 + c], n0 + c_lo + 64 * c, r0);
           }
         }
         __syncwarp();
@@ -437,7 +457,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
 #pragma unroll 1
         for (int c = 0; c < COLS / 64; ++c) {
           uint8_t* buf = rbuf0 + c * 4096;
-          mbar_wait(&rbar[e * 3 + c], (ring >> c) & 1);
+          mbar_wait(&rbar[e * 4 + c], (ring >> c) & 1);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             float v[32];
@@ -521,11 +541,43 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           else
             out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
         }
-      } else if constexpr (KIND == EPI_RES_LN) {
-        // 12 epilogue warps: the 3 warps of a lane quarter split each 384-column
-        // row into 128-column thirds (4 chunks of 32); 32-column chunks are
-        // staged in 64B-swizzled smem and stored by TMA (box 32 x 32).
+      } else if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
+        // RES_LN: 12 epilogue warps; the 3 warps of a lane quarter split each
+        // 384-column row into 128-column thirds.  RES_LN2: this CTA owns a
+        // 192-column slice; 8 warps, 2 per lane quarter (96 columns each), and the
+        // row statistics of the XCH_CL slices meet in distributed shared memory.
+        // Either way 32-column chunks are staged in 64B-swizzled smem and stored by
+        // TMA (box 32 x 32).
         static_assert(KIND != EPI_RES_LN || (EPI_WARPS == 12 && COLS % 32 == 0), "RES_LN layout");
+        static_assert(KIND != EPI_RES_LN2 || (EPI_WARPS == 8 && COLS == 96), "RES_LN2 layout");
+        // row statistic over the whole (384-wide) row from this thread's partial
+        auto row_total = [&](float part, int pass) -> float {
+          if constexpr (KIND == EPI_RES_LN) {
+            const uint32_t eq = e & 3;
+            float* rr = red + pass * EPI_WARPS * 32;
+            rr[e * 32 + lane] = part;
+            named_bar_sync(1 + quarter, 96);
+            return rr[eq * 32 + lane] + rr[(eq + 4) * 32 + lane] + rr[(eq + 8) * 32 + lane];
+          } else {
+            const uint32_t par = local & 1, g = e >> 2, row = quarter * 32 + lane;
+            // xch[par][pass][src][g][row]: push this partial into every cluster peer
+            const uint32_t off = (uint32_t)((((par * 2 + pass) * XCH_CL + crank) * 2 + g) * 128 + row) * 4u;
+#pragma unroll
+            for (uint32_t q = 0; q < (uint32_t)XCH_CL; ++q) st_cluster_f32(mapa_shared(smem_u32(xch) + off, q), part);
+            // each thread releases its own DSMEM stores to every peer (count XCH_CL * EPI_THREADS)
+#pragma unroll
+            for (uint32_t q = 0; q < (uint32_t)XCH_CL; ++q)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&xbar[par * 2 + pass]), q));
+            mbar_wait_cluster(&xbar[par * 2 + pass], (local >> 1) & 1);
+            if (pass == 0 && warp == 2 && lane == 0) GTR(6, local);
+            float tot = 0.f;
+#pragma unroll
+            for (int q = 0; q < XCH_CL; ++q)
+#pragma unroll
+              for (int gg = 0; gg < 2; ++gg) tot += xch[(((par * 2 + pass) * XCH_CL + q) * 2 + gg) * 128 + row];
+            return tot;
+          }
+        };
         const float* vgate = vb + BN + c_lo;
         const float* vshift = vb + 2 * BN + c_lo;
         const float* vscale = vb + 3 * BN + c_lo;
@@ -540,10 +592,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
         float sum = 0.f;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          const uint32_t b = (ring + q) % 3;
-          uint8_t* buf = rbuf0 + b * C::OUT_BUF;
-          mbar_wait(&rbar[e * 3 + b], (rpar >> b) & 1);
-          rpar ^= 1u << b;
+          uint8_t* buf = rbuf0 + q * C::OUT_BUF;
+          mbar_wait(&rbar[e * 4 + q], local & 1);  // one residual load per buffer per tile
           uint4 oldv[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -579,18 +629,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           if (lane == 0) {
             if (st_ok) tma_store_2d(&maps.d[0], buf, n0 + c_lo + 32 * q, r0);
             bulk_commit();
-            if (q + 2 < NQ) {
-              bulk_wait_read<1>();  // the store that last used the next buffer has read it
-              res_load(ring + q + 2, q + 2);
-            }
           }
           __syncwarp();
         }
-        // the 3 warps of this lane quarter hold the 3 thirds of each row
-        const uint32_t eq = e & 3;
-        red[e * 32 + lane] = sum;
-        named_bar_sync(1 + quarter, 96);
-        const float mean = (red[eq * 32 + lane] + red[(eq + 4) * 32 + lane] + red[(eq + 8) * 32 + lane]) * (1.0f / N);
+        const float mean = row_total(sum, 0) * (1.0f / N);
         float var = 0.f;
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
@@ -600,15 +642,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
             const float d0 = xv.x - mean, d1 = xv.y - mean;
             var += d0 * d0 + d1 * d1;
           }
-        float* red2 = red + EPI_WARPS * 32;
-        red2[e * 32 + lane] = var;
-        named_bar_sync(1 + quarter, 96);
-        const float var_all = red2[eq * 32 + lane] + red2[(eq + 4) * 32 + lane] + red2[(eq + 8) * 32 + lane];
+        const float var_all = row_total(var, 1);
         const float rstd = rsqrtf(var_all * (1.0f / N) + ep.ln_eps);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          uint8_t* buf = rbuf0 + ((ring + NQ + q) % 3) * C::OUT_BUF;
-          if (lane == 0) bulk_wait_read<2>();  // the store 3 uses ago left this buffer
+          uint8_t* buf = rbuf0 + q * C::OUT_BUF;
+          if (lane == 0) bulk_wait_read<NQ - 1>();  // the residual store out of buffer q has read it
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -633,10 +672,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
           }
           __syncwarp();
         }
-        ring += 2 * NQ;
       }
     }
-    if (warp == 2 && lane == 0) GTR(5, 0);
     if (lane == 0) bulk_wait<0>();  // all output stores of this warp have landed
     __syncwarp();
   }
@@ -644,6 +681,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if constexpr (CLUSTER) cluster_sync_all();  // no CTA leaves while a peer may still write its smem
 }
 
 }  // namespace sf

@@ -46,9 +46,9 @@ def test_qkv_scatter(rows):
         assert (got.float() - want).abs().max().item() < 2e-2 * max(1.0, want.abs().max().item())
 
 
-@pytest.mark.parametrize("K", [384, 1536])
-def test_res_ln_epilogue(K):
-    rows, T, N = 2, 1024, 384
+@pytest.mark.parametrize("K,rows", [(384, 2), (1536, 2), (1536, 1), (1536, 3)])
+def test_res_ln_epilogue(K, rows):
+    T, N = 1024, 384
     M = rows * T
     g = torch.Generator(device="cuda").manual_seed(K)
     a = bf(torch.randn(M, K, device="cuda", generator=g))

@@ -73,7 +73,7 @@ for n in (256, 512, 1024, 2048):
     print(f"mainloop only N={n} K={D}: {ms*1e3:7.1f} us {2*M*n*D/ms/1e9:7.1f} TFLOP/s")
 import ctypes
 lib = ctypes.CDLL(_lib.LIB_PATH)
-for mode in (1, 2):
+for mode in (3, 4):
     lib.sf_diag_res_ln(mode)
     for name, A, K in (("proj", a, D), ("fc2", h, 4 * D)):
         w2 = bf(torch.randn(D, K, device=dev) * 0.05)
