@@ -24,7 +24,9 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   const int bn = (N % 256 == 0) ? 256 : 128;
   GemmMaps maps;
   if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
-  if (epi != EPI_F32 && make_out_map(&maps.d[0], C, M, N) != SF_OK) return SF_ERR_CUDA;
+  if (epi != EPI_F32 && (gemm_narrow_out(bn, epi) ? make_out_map32(&maps.d[0], C, M, N)
+                                                  : make_out_map(&maps.d[0], C, M, N)) != SF_OK)
+    return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
   ep.out = C;

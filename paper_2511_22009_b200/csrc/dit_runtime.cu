@@ -732,7 +732,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? 192 : 144);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
     rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
-    rc |= make_out_map(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);
+    rc |= make_out_map32(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);  // 256-wide GELU tiles: 32-column chunks
     if (H == 384) {  // RES_LN epilogue: whole rows per tile
       rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
       rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);

@@ -86,7 +86,13 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
 
 template <int BN, int KIND>
 constexpr int epi_warps() {
-  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : 8;  // EPI_RES, EPI_RES_LN2: 8
+  // QKV: 4; RES_LN: 12; bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
+  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+}
+
+// Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).
+int gemm_narrow_out(int bn, int kind) {
+  return (kind == EPI_RES_LN || kind == EPI_RES_LN2 || ((kind == EPI_BF16 || kind == EPI_GELU) && bn == 256)) ? 1 : 0;
 }
 
 template <int BN, int KIND>

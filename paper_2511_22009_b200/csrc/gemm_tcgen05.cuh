@@ -98,7 +98,8 @@ struct GemmCfg {
   // overwritten in place by the updated residual before its TMA store)
   // (head dim 72 QKV, BN = 144: 32 x 144 B Q/K rows or 72 x 64 B V^T rows per buffer)
   static constexpr bool LN_RING = KIND == EPI_RES_LN || KIND == EPI_RES_LN2;  // 32-column SW64 chunks
-  static constexpr int OUT_BUF = BN == 144 ? 5120 : LN_RING ? 2048 : 4096;
+  static constexpr bool NARROW = LN_RING || ((KIND == EPI_BF16 || KIND == EPI_GELU) && EPI_WARPS == 16);
+  static constexpr int OUT_BUF = BN == 144 ? 5120 : NARROW ? 2048 : 4096;
   static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : 2;  // RES_LN(2): one buffer per chunk
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
   static constexpr int RBAR_BYTES = EPI_WARPS * 4 * 8;  // residual-chunk barriers (one per staging buffer)
@@ -111,7 +112,7 @@ struct GemmCfg {
   static_assert(STAGES >= 3, "pipeline too shallow");
   static_assert(MMA_N % 16 == 0 && MMA_N <= 256, "bad MMA N");
   static_assert(B_BOX <= 256, "bad box");
-  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8 || EPI_WARPS == 12, "epilogue warps");
+  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8 || EPI_WARPS == 12 || EPI_WARPS == 16, "epilogue warps");
 };
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -120,6 +121,19 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   float t;
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
   return 0.5f * x * (1.0f + t);
+}
+
+// tanh-GELU of a pair: packed f32x2 arithmetic (FFMA2/FMUL2) around two MUFU.TANH.
+__device__ __forceinline__ float2 gelu_tanh2(float2 x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 t = __ffma2_rn(x2, make_float2(k0 * k1, k0 * k1), make_float2(k0, k0));  // k0 (1 + k1 x^2)
+  const float2 u = __fmul2_rn(x, t);
+  float2 th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th.x) : "f"(u.x));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th.y) : "f"(u.y));
+  const float2 h = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+  return __ffma2_rn(h, th, h);  // 0.5 x (1 + tanh u)
 }
 
 __device__ __forceinline__ uint4 pack8_bf16(const float* v) {
@@ -375,6 +389,31 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
+      } else if constexpr ((KIND == EPI_BF16 || KIND == EPI_GELU) && C::NARROW) {
+        // 16 epilogue warps (4 per TMEM lane quarter): 32-column chunks, 64B-swizzled
+        // staging (box 32 x 32), bias + GELU in packed f32x2 arithmetic
+#pragma unroll 1
+        for (int c0 = 0; c0 < COLS; c0 += 32) {
+          uint8_t* buf = out.acquire(lane);
+          float v[32];
+          tmem_ld32(taddr + c_lo + c0, v);
+          tmem_ld_wait();
+          if (c0 + 32 >= COLS) {  // last TMEM read of this tile by this warp
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 bb = reinterpret_cast<const float2*>(vbias + c0)[i];
+            float2 y = __fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), bb);
+            if constexpr (KIND == EPI_GELU) y = gelu_tanh2(y);
+            v[2 * i] = y.x;
+            v[2 * i + 1] = y.y;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, i, pack8_bf16(v + 8 * i));
+          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
+        }
       } else if constexpr (KIND == EPI_BF16 || KIND == EPI_GELU) {
 #pragma unroll 1
         for (int c0 = 0; c0 < COLS; c0 += 64) {

@@ -16,6 +16,7 @@ int gemm_b_box_rows(int bn);
 int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn);
 int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
 int make_out_map32(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
+int gemm_narrow_out(int bn, int kind);
 int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt, int64_t rows, int heads, int T,
                       int hd);
 int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const float* shift, const float* scale,
