@@ -284,7 +284,10 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(dom)
+            t = json.load(fh).get(dom)
+            # dram__bytes_read.sum + dram__bytes_write.sum of one launch (ncu --set full capture)
+            traffic = None if t is None else {"bytes_per_launch": t["per_launch_MB"] * 1e6,
+                                              "source": "profiles/ncu_traffic.json"}
     except Exception:
         pass
     launches_per_step = sum(c for _, c in prof.values())
