@@ -286,8 +286,7 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             t = json.load(fh).get(dom)
             # dram__bytes_read.sum + dram__bytes_write.sum of one launch (ncu --set full capture)
-            traffic = None if t is None else {"bytes_per_launch": t["per_launch_MB"] * 1e6,
-                                              "source": "profiles/ncu_traffic.json"}
+            traffic = None if t is None else t["per_launch_MB"] * 1e6
     except Exception:
         pass
     launches_per_step = sum(c for _, c in prof.values())
@@ -326,7 +325,9 @@ def main():
                     "d2h_bytes_per_step": S * cfg.dim * 4},
             "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": burst, "unit": "TFLOP/s", "frac": round(achieved / burst, 4),
-                         "traffic": traffic, "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
+                         "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write, ncu --set full; "
+                                                             "profiles/ncu_traffic.json)",
+                         "peak_source": f"{src} bf16 burst (MEASURED_PEAKS.json)",
                          "flops_per_launch": flops[dom] / max(dom_n, 1), "launches_per_step": dom_n},
             "step_roofline": {"achieved_tflops": round(step_flops / (total_ms / args.steps / 1e3) / 1e12, 1),
                               "peak": sustained, "frac": round(step_flops / (total_ms / args.steps / 1e3) / 1e12
