@@ -15,6 +15,15 @@ int sf_device_sm_count(void) {
   return n;
 }
 
+// 2-SM (cta_group::2) pair tiles for the bf16/GELU (BN = 256) and QKV (head dim 64) GEMMs:
+// off by default (the single-CTA kernels are faster end to end: the pair main loop alone is
+// ~6% faster but the coupled epilogues lose more); sf_diag_gemm_2sm(1) selects them (diagnostics).
+static int g_gemm_2sm = 0;
+int sf_diag_gemm_2sm(int on) {
+  g_gemm_2sm = on;
+  return 0;
+}
+
 int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
                  int32_t epi, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % 128) return SF_ERR_PARAMETER;
@@ -22,8 +31,10 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   epi &= 0xff;
   if (epi < EPI_F32 || epi > EPI_GELU) return SF_ERR_PARAMETER;
   const int bn = (N % 256 == 0) ? 256 : 128;
+  const bool two = g_gemm_2sm && bn == 256 && (epi == EPI_BF16 || epi == EPI_GELU);
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if ((two ? make_operand_maps_2sm(&maps, A, M, K, W, N, bn) : make_operand_maps(&maps, A, M, K, W, N, bn)) != SF_OK)
+    return SF_ERR_CUDA;
   if (epi != EPI_F32 && (gemm_narrow_out(bn, epi) ? make_out_map32(&maps.d[0], C, M, N)
                                                   : make_out_map(&maps.d[0], C, M, N)) != SF_OK)
     return SF_ERR_CUDA;
@@ -34,6 +45,7 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   ep.tokens_per_slot = 1 << 30;
   ep.M = (int)M;
   ep.no_store = no_store;
+  if (two) return launch_gemm_2sm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
   return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
@@ -42,8 +54,10 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   const int bn = hd == 64 ? 192 : 144;
   const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
   if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
+  const bool two = g_gemm_2sm && hd == 64;
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if ((two ? make_operand_maps_2sm(&maps, A, M, K, W, N, bn) : make_operand_maps(&maps, A, M, K, W, N, bn)) != SF_OK)
+    return SF_ERR_CUDA;
   if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
@@ -51,6 +65,7 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   ep.q_scale = q_scale;
   ep.tokens_per_slot = T;
   ep.M = (int)M;
+  if (two) return launch_gemm_2sm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
   return launch_gemm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 

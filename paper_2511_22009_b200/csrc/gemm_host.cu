@@ -45,6 +45,14 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 int gemm_bk(int bn) { return bn > 256 ? 32 : 64; }
 int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
 
+// 2-SM pair tiles: each CTA loads BN/2 rows of W per stage.
+int make_operand_maps_2sm(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
+  const int bk = gemm_bk(bn);
+  int rc = make_tmap_bf16_2d(&m->a, A, K, M, K, bk, 128, 2 * bk);
+  rc |= make_tmap_bf16_2d(&m->b, W, K, N, K, bk, bn / 2, 2 * bk);
+  return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
+}
+
 int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
   const int bk = gemm_bk(bn);
   int rc = make_tmap_bf16_2d(&m->a, A, K, M, K, bk, 128, 2 * bk);
@@ -112,6 +120,23 @@ static int set_attr() {
   return SF_OK;
 }
 
+template <int BN, int KIND>
+static int set_attr_2sm() {
+  static bool done = false;
+  if (!done) {
+    constexpr int W = epi_warps<BN, KIND>();
+    const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W, 2>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 GemmCfg<BN, W, KIND, 2>::SMEM_BYTES);
+    if (err != cudaSuccess) {
+      fprintf(stderr, "streamflow: gemm2sm<%d,%d> smem attribute failed: %s\n", BN, KIND, cudaGetErrorString(err));
+      return SF_ERR_CUDA;
+    }
+    done = true;
+  }
+  return SF_OK;
+}
+
 // Set every instantiation's smem attribute up front (never inside a graph capture).
 int prepare_gemm_kernels() {
   int rc = SF_OK;
@@ -126,6 +151,9 @@ int prepare_gemm_kernels() {
   rc |= set_attr<144, EPI_QKV>();
   rc |= set_attr<128, EPI_RES>();
   rc |= set_attr<192, EPI_RES_LN2>();
+  rc |= set_attr_2sm<256, EPI_GELU>();
+  rc |= set_attr_2sm<256, EPI_BF16>();
+  rc |= set_attr_2sm<192, EPI_QKV>();
   return rc;
 }
 
@@ -178,6 +206,46 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
     return SF_ERR_CUDA;
   }
   return SF_OK;
+}
+
+template <int BN, int KIND>
+static int launch_one_2sm(const GemmMaps& maps, int M, int N, int K, const EpiParams& ep, cudaStream_t st) {
+  constexpr int W = epi_warps<BN, KIND>();
+  using C = GemmCfg<BN, W, KIND, 2>;
+  if (K % C::BK) return SF_ERR_PARAMETER;
+  if (set_attr_2sm<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
+  const int pairs = ((M + C::BM - 1) / C::BM + 1) / 2 * (N / BN), max_cl = sm_count() / 2;
+  EpiParams e = ep;
+  e.M = M;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * (pairs < max_cl ? pairs : max_cl)));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W, 2>, maps, N, K, e);
+  if (err == cudaSuccess) err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    fprintf(stderr, "streamflow: gemm2sm<%d,%d> launch failed: %s\n", BN, KIND, cudaGetErrorString(err));
+    return SF_ERR_CUDA;
+  }
+  return SF_OK;
+}
+
+// 2-SM (cta_group::2) pair tiles 256 x bn; maps from make_operand_maps_2sm.
+int launch_gemm_2sm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
+                    cudaStream_t st) {
+  if (K % 64 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
+  if (bn == 256 && kind == EPI_GELU) return launch_one_2sm<256, EPI_GELU>(maps, M, N, K, ep, st);
+  if (bn == 256 && kind == EPI_BF16) return launch_one_2sm<256, EPI_BF16>(maps, M, N, K, ep, st);
+  if (bn == 192 && kind == EPI_QKV) return launch_one_2sm<192, EPI_QKV>(maps, M, N, K, ep, st);
+  return SF_ERR_PARAMETER;
 }
 
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,

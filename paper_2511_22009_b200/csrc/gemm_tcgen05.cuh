@@ -20,6 +20,9 @@
 
 namespace sf {
 
+#ifndef SF_GEMM_L2HINT
+#define SF_GEMM_L2HINT 0  // experiment: evict-first output stores, evict-last weight loads
+#endif
 #ifndef SF_GEMM_TRACE
 #define SF_GEMM_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_gemm_trace_read)
 #endif
@@ -76,17 +79,20 @@ struct GemmMaps {
   CUtensorMap a, b, d[3];
 };
 
-template <int BN, int EPI_WARPS, int KIND>
+template <int BN, int EPI_WARPS, int KIND, int CTAS = 1>
 struct GemmCfg {
   static constexpr int BM = 128;
   static constexpr int BK = BN > 256 ? 32 : 64;  // K elements per stage (64 B / 128 B rows)
   static constexpr int SWZ = BK * 2;             // swizzle width of the operand tiles (bytes)
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  // CTAS = 2: a cluster pair computes a 256 x BN tile with cta_group::2 MMAs; each CTA
+  // holds its 128 A rows and BN/2 B rows (the pair MMA reads B from both)
+  static constexpr int B_ROWS = BN / CTAS;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int MMA_N = BN > 256 ? BN / 2 : BN;  // UMMA N <= 256
   static constexpr int N_SPLIT = BN / MMA_N;
-  static constexpr int B_BOX = BN > 256 ? BN / 2 : BN;  // TMA box rows <= 256
+  static constexpr int B_BOX = B_ROWS > 256 ? B_ROWS / 2 : B_ROWS;  // TMA box rows <= 256
   static constexpr int ACC_STAGES = 2 * BN <= 512 ? 2 : 1;
   static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;  // column offset between accumulator stages
   static constexpr int TMEM_COLS = ACC_STAGES == 2 ? (BN <= 128 ? 256 : 512) : (BN <= 256 ? 256 : 512);
@@ -171,17 +177,25 @@ struct OutStageT {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      if (store) tma_store_2d(map, buf, c0, c1);
+      if (store) {
+#if SF_GEMM_L2HINT
+        tma_store_2d_hint(map, buf, c0, c1, l2_policy_evict_first());
+#else
+        tma_store_2d(map, buf, c0, c1);
+#endif
+      }
       bulk_commit();
     }
     ++count;
   }
 };
 
-template <int BN, int KIND, int EPI_WARPS>
-__global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
+template <int BN, int KIND, int EPI_WARPS, int CTAS = 1>
+__global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ GemmMaps maps, int N, int K, EpiParams ep) {
-  using C = GemmCfg<BN, EPI_WARPS, KIND>;
+  using C = GemmCfg<BN, EPI_WARPS, KIND, CTAS>;
+  constexpr bool TWO_SM = CTAS == 2;
+  static_assert(!TWO_SM || (BN <= 256 && KIND != EPI_RES_LN2), "2-SM tiles: BN <= 256");
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array (keeps the pointer in the shared window: LDS/STS, not generic)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -209,12 +223,25 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
   const int num_kb = K / C::BK;
   // Tile sequence: default = all (m, n) tiles N-fastest over the grid; cluster mode =
   // the cluster walks row tiles m, CTA rank r of the cluster owns column slice n = r.
-  const uint32_t crank = CLUSTER ? cluster_ctarank() : 0u;
-  const int t_first = CLUSTER ? (int)(blockIdx.x / XCH_CL) : (int)blockIdx.x;
-  const int t_stride = CLUSTER ? (int)(gridDim.x / XCH_CL) : (int)gridDim.x;
-  const int t_limit = CLUSTER ? num_m : total;
-  auto tile_m0 = [&](int tile) { return CLUSTER ? tile * C::BM : (tile / num_n) * C::BM; };
+  // 2-SM mode: the pair walks (row-pair, n) tiles, CTA rank r owns rows 2*pair + r.
+  const uint32_t crank = (CLUSTER || TWO_SM) ? cluster_ctarank() : 0u;
+  const bool leader = crank == 0;
+  const int num_mp = (num_m + 1) / 2;
+  const int t_first = CLUSTER ? (int)(blockIdx.x / XCH_CL) : TWO_SM ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
+  const int t_stride = CLUSTER ? (int)(gridDim.x / XCH_CL) : TWO_SM ? (int)(gridDim.x / 2) : (int)gridDim.x;
+  const int t_limit = CLUSTER ? num_m : TWO_SM ? num_mp * num_n : total;
+  auto tile_m0 = [&](int tile) {
+    return CLUSTER ? tile * C::BM : TWO_SM ? (2 * (tile / num_n) + (int)crank) * C::BM : (tile / num_n) * C::BM;
+  };
   auto tile_n0 = [&](int tile) { return CLUSTER ? (int)crank * BN : (tile % num_n) * BN; };
+  // epilogue -> MMA accumulator release (2-SM: both CTAs' epilogues arrive on the leader's barrier)
+  auto acc_release = [&](uint32_t a) {
+    tc_fence_before();
+    if constexpr (TWO_SM)
+      mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[a]), 0));
+    else
+      mbar_arrive(&tempty[a]);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a);
@@ -225,7 +252,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
     }
     for (int a = 0; a < C::ACC_STAGES; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS * 32);
+      mbar_init(&tempty[a], CTAS * EPI_WARPS * 32);
     }
     if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES || KIND == EPI_RES_LN2)
       for (int i = 0; i < EPI_WARPS * 4; ++i) mbar_init(&rbar[i], 1);
@@ -233,8 +260,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
       for (int i = 0; i < 4; ++i) mbar_init(&xbar[i], XCH_CL * EPI_WARPS * 32);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
-  if constexpr (CLUSTER) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
+  if (warp == 1) {
+    if constexpr (TWO_SM)
+      tmem_alloc_2sm<C::TMEM_COLS>(tmem_holder);
+    else
+      tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  }
+  if constexpr (CLUSTER || TWO_SM) cluster_sync_all();  // peers' barriers initialised before any remote arrive
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -249,12 +281,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
+          if constexpr (TWO_SM) {
+            // both CTAs' operand bytes land on the leader's full barrier
+            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+            if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+            tma_load_2d_2sm(sA + s * C::A_BYTES, &maps.a, fb, kb * C::BK, m0);
+            tma_load_2d_2sm(sB + s * C::B_BYTES, &maps.b, fb, kb * C::BK, n0 + (int)crank * C::B_ROWS);
+            continue;
+          }
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
           tma_load_2d(sA + s * C::A_BYTES, &maps.a, &full[s], kb * C::BK, m0);
 #pragma unroll
-          for (int h = 0; h < BN / C::B_BOX; ++h)
+          for (int h = 0; h < BN / C::B_BOX; ++h) {
+#if SF_GEMM_L2HINT
+            tma_load_2d_hint(sB + s * C::B_BYTES + h * C::B_BOX * C::SWZ, &maps.b, &full[s], kb * C::BK,
+                             n0 + h * C::B_BOX, l2_policy_evict_last());
+#else
             tma_load_2d(sB + s * C::B_BYTES + h * C::B_BOX * C::SWZ, &maps.b, &full[s], kb * C::BK,
                         n0 + h * C::B_BOX);
+#endif
+          }
         }
       }
     }
@@ -262,11 +308,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
     // ---------------- MMA issuer: the whole warp runs the loop so descriptors
     // stay warp-uniform (uniform registers, no per-MMA R2UR waterfall); one
     // elected lane issues.  Descriptor address field = addr >> 4.
-    constexpr uint32_t idesc = idesc_bf16_f32(128, C::MMA_N);
+    constexpr uint32_t idesc = idesc_bf16_f32(TWO_SM ? 256 : 128, C::MMA_N);
     const uint64_t a_desc0 = kmajor_desc<C::SWZ>(smem_u32(sA));
     const uint64_t b_desc0 = kmajor_desc<C::SWZ>(smem_u32(sB));
     uint32_t it = 0, local = 0;
-    for (int tile = t_first; tile < t_limit; tile += t_stride, ++local) {
+    for (int tile = t_first; tile < ((TWO_SM && !leader) ? t_first : t_limit); tile += t_stride, ++local) {
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
@@ -279,15 +325,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
         const uint64_t ad = a_desc0 + (uint64_t)((s * C::A_BYTES) >> 4);
         const uint64_t bd = b_desc0 + (uint64_t)((s * C::B_BYTES) >> 4);
         if (elect_one()) {
+          if constexpr (TWO_SM) {
 #pragma unroll
-          for (int k = 0; k < C::BK / 16; ++k) {
+            for (int k = 0; k < C::BK / 16; ++k) mma_bf16_ss_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_2sm_mc(&empty[s], 0x3);                     // both CTAs may refill stage s
+            if (kb + 1 == num_kb) mma_commit_2sm_mc(&tfull[acc], 0x3);  // both epilogues may start
+          } else {
 #pragma unroll
-            for (int h = 0; h < C::N_SPLIT; ++h)
-              mma_bf16_ss(d + h * C::MMA_N, ad + 2 * k, bd + (uint64_t)((h * C::MMA_N * C::SWZ) >> 4) + 2 * k, idesc,
-                          (kb | k) != 0);
+            for (int k = 0; k < C::BK / 16; ++k) {
+#pragma unroll
+              for (int h = 0; h < C::N_SPLIT; ++h)
+                mma_bf16_ss(d + h * C::MMA_N, ad + 2 * k, bd + (uint64_t)((h * C::MMA_N * C::SWZ) >> 4) + 2 * k,
+                            idesc, (kb | k) != 0);
+            }
+            mma_commit(&empty[s]);
+            if (kb + 1 == num_kb) mma_commit(&tfull[acc]);
           }
-          mma_commit(&empty[s]);
-          if (kb + 1 == num_kb) mma_commit(&tfull[acc]);
         }
         __syncwarp();
       }
@@ -365,8 +418,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
       tc_fence_after();
       if (warp == 2 && lane == 0) GTR(3, local);
       if (ep.no_store == 2) {  // diagnostics: main loop only
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        acc_release(acc);
         continue;
       }
       const float* vbias = vb + c_lo;
@@ -387,8 +439,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        acc_release(acc);
       } else if constexpr ((KIND == EPI_BF16 || KIND == EPI_GELU) && C::NARROW) {
         // 16 epilogue warps (4 per TMEM lane quarter): 32-column chunks, 64B-swizzled
         // staging (box 32 x 32), bias + GELU in packed f32x2 arithmetic
@@ -399,8 +450,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
           tmem_ld32(taddr + c_lo + c0, v);
           tmem_ld_wait();
           if (c0 + 32 >= COLS) {  // last TMEM read of this tile by this warp
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            acc_release(acc);
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -439,8 +489,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
             for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, 4 * h + i, pack8_bf16(v + 8 * i));
           }
           if (c0 + 64 >= COLS) {  // last TMEM read of this tile by this warp
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            acc_release(acc);
           }
           out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
         }
@@ -465,8 +514,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
           tmem_ld16(taddr + 72 * hh + 64, *reinterpret_cast<float(*)[16]>(&v[64]));
           tmem_ld_wait();
           if (hh == 1) {
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            acc_release(acc);
           }
 #pragma unroll
           for (int i = 0; i < 18; ++i) {
@@ -503,8 +551,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
             tmem_ld32(taddr + c_lo + 64 * c + 32 * h, v);
             tmem_ld_wait();
             if (c + 1 == COLS / 64 && h == 1) {
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
+              acc_release(acc);
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -525,7 +572,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (st_ok) tma_store_2d(&maps.d[0], buf, n0 + c_lo + 64 * c, r0);
+            if (st_ok) {
+#if SF_GEMM_L2HINT
+              tma_store_2d_hint(&maps.d[0], buf, n0 + c_lo + 64 * c, r0, l2_policy_evict_first());
+#else
+              tma_store_2d(&maps.d[0], buf, n0 + c_lo + 64 * c, r0);
+#endif
+            }
             bulk_commit();
           }
           __syncwarp();
@@ -572,8 +625,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
             }
           }
           if (c0 + 64 >= COLS) {
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            acc_release(acc);
           }
           if (which < 2)
             out.release(lane, &maps.d[which], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
@@ -645,8 +697,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
             tmem_ld16(tcol + 16 * u, v);
             tmem_ld_wait();
             if (u + 1 == 2 * NQ) {  // last TMEM read: the next tile's main loop may start
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
+              acc_release(acc);
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -719,7 +770,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND>::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if constexpr (TWO_SM) cluster_sync_all();  // the pair's MMAs / barrier traffic are over
+  if (warp == 1) {
+    if constexpr (TWO_SM)
+      tmem_dealloc_2sm<C::TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
   if constexpr (CLUSTER) cluster_sync_all();  // no CTA leaves while a peer may still write its smem
 }
 

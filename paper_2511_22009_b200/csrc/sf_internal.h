@@ -25,6 +25,9 @@ int prepare_gemm_kernels();
 int prepare_attn_kernel();
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
                 cudaStream_t st);
+int make_operand_maps_2sm(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn);
+int launch_gemm_2sm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
+                    cudaStream_t st);
 
 struct AttnMaps {
   CUtensorMap q, qh, k, kh, v;  // qh/kh: head-dim elements 64..79 (head dim 72 only)

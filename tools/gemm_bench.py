@@ -9,7 +9,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_22009_b200 import _lib  # noqa: E402
 
-M = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
+M = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 131072
+if "--2sm" in sys.argv:  # cta_group::2 pair tiles for fc1 / QKV (off by default)
+    import ctypes
+    ctypes.CDLL(_lib.LIB_PATH).sf_diag_gemm_2sm(1)
 T, H, D = 1024, 6, 384
 st = torch.cuda.current_stream().cuda_stream
 bf = lambda t: t.to(torch.bfloat16)
