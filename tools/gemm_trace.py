@@ -30,6 +30,6 @@ lib = ctypes.CDLL(_lib.LIB_PATH)
 assert lib.sf_gemm_trace_read(buf.ctypes.data_as(ctypes.c_void_p)) == 0
 tr = buf.reshape(8, 64)
 t0 = tr[0, 0]
-print("tile  mma_start  mma_issued  epi_ready  epi_got_acc  before_bar  after_bar  after_wait  cta1_after_bar(own clock)")
+print("tile  mma_start  mma_issued  epi_ready  epi_got_acc   (cycles; mma_issued = last MMA of the tile issued)")
 for i in range(12):
-    print(f"{i:4d} " + " ".join(f"{(tr[r, i] - t0) if tr[r, i] else -1:11d}" for r in (0, 1, 2, 3, 4, 5, 6, 7)))
+    print(f"{i:4d} " + " ".join(f"{(tr[r, i] - t0) if tr[r, i] else -1:11d}" for r in (0, 1, 2, 3)))
