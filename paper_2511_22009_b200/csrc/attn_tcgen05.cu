@@ -32,6 +32,13 @@
 #include "sf_internal.h"
 #include "sf_ptx.cuh"
 
+#ifndef SF_ATTN_NOEXP
+#define SF_ATTN_NOEXP 0  // diagnostics: 1 = skip exp2 (timing only, wrong results), 2 = all MUFU,
+                         // 3 = softmax skipped (MMA/sync skeleton), 4 = no MMAs
+#endif
+#ifndef SF_ATTN_QTMEM
+#define SF_ATTN_QTMEM 1  // head dim 64: Q staged in TMEM (tcgen05.cp), S MMA in TS form
+#endif
 #ifndef SF_ATTN_TRACE
 #define SF_ATTN_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_attn_trace_read)
 #endif
@@ -64,6 +71,9 @@ constexpr int TMEM_COLS = 512;
 __host__ __device__ constexpr uint32_t S_COL(int t, int b) { return 64u * (2 * t + b); }
 __host__ __device__ constexpr uint32_t P_COL(int t, int b) { return 64u * (2 * t + b) + 32u; }
 __host__ __device__ constexpr uint32_t O_COL(int t) { return 256u + 128u * t; }
+// head dim 64: Q_t is copied into TMEM (tcgen05.cp) and the S MMA reads it from there,
+// so K is the only shared-memory operand of QK^T (halves its smem traffic)
+__host__ __device__ constexpr uint32_t Q_COL(int t) { return 352u + 128u * t; }
 constexpr int THREADS = 352;
 }  // namespace attn
 
@@ -126,6 +136,11 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 }
 
 // D[tmem] (+)= A[tmem] * B[smem]^T (A operand read from TMEM, "TS" form).
+// smem -> TMEM copy of a 128-row x 32-byte block described by an smem matrix descriptor.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
@@ -144,6 +159,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
                      int nitems) {
   using namespace attn;
   using AC = AttnCfg<HD>;
+  constexpr bool Q_IN_TMEM = HD == 64 && SF_ATTN_QTMEM;
   constexpr int Q_TILE = AC::Q_TILE, Q_BYTES = AC::Q_BYTES, K_BYTES = AC::K_BYTES, STAGE = AC::STAGE;
   constexpr int V_ROWS = AC::V_ROWS, V_TMA = AC::V_TMA;
   extern __shared__ uint8_t smem_raw[];
@@ -250,8 +266,14 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       const uint64_t qd = q_desc0 + (uint64_t)((qb * Q_BYTES) >> 4);
       const uint64_t kd = kv_desc0 + (uint64_t)((s * STAGE) >> 4);
       if (elect_one()) {
+        if constexpr (SF_ATTN_NOEXP == 4) {  // diagnostics: no MMAs (softmax/sync alone)
+        } else if constexpr (Q_IN_TMEM) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + S_COL(t, b), qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+          for (int k = 0; k < 4; ++k) mma_f16_ts(tmem + S_COL(t, b), tmem + Q_COL(t) + 8 * k, kd + 2 * k, idesc_s, k != 0);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + S_COL(t, b), qd + 2 * k, kd + 2 * k, idesc_s, k != 0);
+        }
         if constexpr (AC::HI > 0)  // head-dim elements 64..79 from the SW32 parts
           mma_bf16_ss(tmem + S_COL(t, b), sw32_kmajor_desc(smem_u32(sQ + qb * Q_BYTES + t * Q_TILE + AC::Q_LO)),
                       sw32_kmajor_desc(smem_u32(sKV + s * STAGE + AC::K_LO)), idesc_s, 1);
@@ -264,7 +286,8 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, vd + 2 * k, idesc_pv, acc || k != 0);
+          if (SF_ATTN_NOEXP != 4)
+            mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, vd + 2 * k, idesc_pv, acc || k != 0);
         mma_commit(&o_full[2 * t + b]);
         mma_commit(&kv_empty[s]);
       }
@@ -274,6 +297,18 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++local) {
       const int qb = local & 1;
       mbar_wait(&q_full[qb], (local >> 1) & 1);
+      if constexpr (Q_IN_TMEM) {
+        // the previous item's last S on this tile (buffer 1) has finished reading Q_t in TMEM
+        if (kv > 0) mbar_wait(&s_full[2 * t + 1], ((kv - 1) >> 1) & 1);
+        tc_fence_after();
+        const uint64_t qd = q_desc0 + (uint64_t)((qb * Q_BYTES) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tmem_cp_128x256b(tmem + Q_COL(t) + 8 * k, qd + 2 * k);
+          mma_commit(&q_empty[qb]);  // Q smem buffer free once the copy has read it
+        }
+        __syncwarp();
+      }
       for (int j = 0; j < 2; ++j) {
         const int G = kv + j;
         mbar_wait(&kv_full[G % KV_STAGES], (G / KV_STAGES) & 1);
@@ -294,7 +329,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
           tc_fence_after();
           if (lane == 0) ATR(5 + 2 * t, G + 2);
           issue_s(qb, (G + 2) % KV_STAGES, b);
-          if (j + 3 == nkv) {
+          if (!Q_IN_TMEM && j + 3 == nkv) {
             if (elect_one()) mma_commit(&q_empty[qb]);  // last S of this tile on this Q
             __syncwarp();
           }
@@ -320,6 +355,10 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         mbar_wait(&s_full[2 * t + b], (G >> 1) & 1);
         if (lane == 0 && quarter == 0) ATR(2 * t, G);
         tc_fence_after();
+#if SF_ATTN_NOEXP == 3  // diagnostics: softmax does no work (MMA/sync skeleton alone)
+        mbar_arrive(&p_full[2 * t + b]);
+        continue;
+#endif
         float s[BKV];
         tmem_ld32(lane_base + S_COL(t, b), *reinterpret_cast<float(*)[32]>(&s[0]));
         tmem_ld32(lane_base + S_COL(t, b) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
@@ -365,12 +404,19 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
           for (int i = 0; i < 16; ++i) {
             const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), l2e2, negm);
             float2 p;
+#if SF_ATTN_NOEXP == 1
+            p = x;  // diagnostics: no exponentials (timing only)
+#elif SF_ATTN_NOEXP == 2
+            p.x = ex2(x.x);
+            p.y = ex2(x.y);
+#else
             if (i < SF_ATTN_EMU_PAIRS) {
               p = exp2_poly2(x);
             } else {
               p.x = ex2(x.x);
               p.y = ex2(x.y);
             }
+#endif
             pk[i] = pack_f16(p.x, p.y);
           }
           tmem_st16u(lane_base + P_COL(t, b) + 16 * c, pk);
