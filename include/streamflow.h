@@ -268,6 +268,13 @@ int sf_dit_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, float* x_
 /* On-device N(0,1) noise: out[s, i] = Philox(seed + s, gen, i) (Box-Muller). */
 int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t gen, void* stream);
 
+/* numpy-identical generation noise (replaces the host call of
+ * generation_noise, src/pipeline.py:92-98 -> np.random.default_rng([seed, gen])
+ * .standard_normal(D)): out[s, :] = those D draws for seeds[s] (device int64 [S],
+ * each >= 0), bit-identical in fp64 (out_dtype SF_F64) or their round-to-nearest
+ * fp32 cast (SF_F32, pipeline.py:176).  gen >= 0. */
+int sf_numpy_normal(const int64_t* seeds, int64_t gen, int64_t S, int64_t D, void* out, int out_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

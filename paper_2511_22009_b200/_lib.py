@@ -58,6 +58,7 @@ SIGNATURES = {
     "sf_analytic_eps": [_vp, _vp, _vp, C.c_int, _vp, _i64, _i64, _vp, _vp],
     "sf_attention": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
     "sf_attention_hd": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp],
+    "sf_numpy_normal": [_vp, _i64, _i64, _i64, _vp, C.c_int, _vp],
 }
 
 _lib = None

@@ -95,6 +95,31 @@ def generation_noise(seed: int, gen_id: int, dim: int) -> np.ndarray:
     return np.random.default_rng([seed, gen_id]).standard_normal(dim)
 
 
+def numpy_noise_device(seeds, gen: int, dim: int, dtype=torch.float64, out: torch.Tensor | None = None,
+                       device: str = "cuda") -> torch.Tensor:
+    """generation_noise for every seed at once, on the device: row s of the result is
+    bit-identical to ``np.random.default_rng([seeds[s], gen]).standard_normal(dim)``
+    (cast to fp32 with round-to-nearest when dtype is float32, as pipeline.py:176 does).
+    sf_numpy_normal: SeedSequence -> PCG64 -> numpy's ziggurat on the GPU."""
+    if isinstance(seeds, torch.Tensor) and seeds.is_cuda:
+        sd = seeds.to(torch.int64).contiguous()
+    else:
+        vals = [int(v) for v in (seeds if isinstance(seeds, (list, tuple)) else np.asarray(seeds).ravel())]
+        if any(v < 0 for v in vals) or gen < 0:
+            raise ValueError("expected non-negative integer")  # numpy's SeedSequence error
+        if any(v >= 1 << 63 for v in vals):
+            raise ParameterError("seeds must be < 2**63 for the device generator")
+        sd = torch.tensor(vals, dtype=torch.int64, device=device)
+    S = sd.numel()
+    if out is None:
+        out = torch.empty(S, dim, dtype=dtype, device=sd.device)
+    if out.shape != (S, dim) or not out.is_contiguous() or out.dtype not in (torch.float32, torch.float64):
+        raise ParameterError("out must be a contiguous [S, dim] float32/float64 tensor")
+    _lib.call("sf_numpy_normal", sd.data_ptr(), int(gen), S, int(dim), out.data_ptr(),
+              _lib.SF_F64 if out.dtype == torch.float64 else _lib.SF_F32, torch.cuda.current_stream().cuda_stream)
+    return out
+
+
 def _check_run_args(m: int, n: int, sched: TimeWindowSchedule) -> None:
     if m < 1:
         raise ParameterError(f"need at least one generation, got m={m}")
@@ -119,8 +144,12 @@ class StreamBatch:
     seed       run seed of stream 0 (stream s uses seed + s) or a list of S
     m          generations per stream (None = unbounded serving)
     dtype      latent dtype (np.float64 / np.float32; the DiT keeps fp32)
-    noise      "numpy": generation_noise (bit-identical to the reference),
-               "device": on-device Philox N(0,1) (throughput mode)
+    noise      "numpy": generation_noise bit-identical to the reference, drawn on
+                        the device (sf_numpy_normal: SeedSequence/PCG64/ziggurat),
+               "numpy_host": the same noise computed by numpy on the host and
+                        uploaded (cross-check path),
+               "device": on-device Philox N(0,1) (throughput mode),
+               "host":  caller-provided noise via launch_host_io
     """
 
     def __init__(self, model: VelocityModel, sched: TimeWindowSchedule, n: int, num_streams: int = 1,
@@ -131,8 +160,8 @@ class StreamBatch:
         _check_run_args(1 if m is None else m, n, sched)
         if num_streams < 1:
             raise ParameterError(f"need at least one stream, got {num_streams}")
-        if noise not in ("numpy", "device", "host"):
-            raise ParameterError(f"noise must be 'numpy', 'device' or 'host', got {noise!r}")
+        if noise not in ("numpy", "numpy_host", "device", "host"):
+            raise ParameterError(f"noise must be 'numpy', 'numpy_host', 'device' or 'host', got {noise!r}")
         self.model, self.sched, self.n, self.S = model, sched, int(n), int(num_streams)
         self.m = _UNBOUNDED if m is None else int(m)
         self.noise, self.use_graph, self.device = noise, bool(use_graph), device
@@ -177,8 +206,14 @@ class StreamBatch:
             np.stack([np.zeros(E) if x is None else x for x in negs]), dtype=torch.float64).to(dev).contiguous()
         noise_dt = torch.float32 if self.kind == "dit" else torch.float64
         self.noise_dev = torch.zeros(self.S, self.D, dtype=noise_dt, device=dev)
-        self.noise_host = torch.zeros(self.S, self.D, dtype=noise_dt).pin_memory() if noise == "numpy" else None
+        self.noise_host = torch.zeros(self.S, self.D, dtype=noise_dt).pin_memory() if noise == "numpy_host" else None
         self.noise_seed = int(self.seeds[0]) & ((1 << 64) - 1)
+        if noise == "numpy":
+            if any(int(v) < 0 for v in self.seeds):
+                raise ValueError("expected non-negative integer")  # numpy's SeedSequence error
+            if any(int(v) >= 1 << 63 for v in self.seeds):
+                raise ParameterError("seeds must be < 2**63 for the device generator")
+            self.seeds_dev = torch.tensor([int(v) for v in self.seeds], dtype=torch.int64, device=dev)
         self._h2d_done = torch.cuda.Event()
         self.stats = [RunStats() for _ in range(self.S)]
         self.j = 0
@@ -191,6 +226,8 @@ class StreamBatch:
         if gen >= self.m:
             return False
         if self.noise == "numpy":
+            numpy_noise_device(self.seeds_dev, gen, self.D, out=self.noise_dev)
+        elif self.noise == "numpy_host":
             arr = np.stack([generation_noise(sd, gen, self.D) for sd in self.seeds])
             self._h2d_done.synchronize()  # the previous async copy has left the pinned buffer
             self.noise_host.copy_(torch.from_numpy(arr.astype(self.noise_host.numpy().dtype, copy=False)))
@@ -203,7 +240,7 @@ class StreamBatch:
         self.j = 0
         self.stats = [RunStats() for _ in range(self.S)]
         self._fill_noise(0)
-        use_host = self.noise == "numpy"
+        use_host = self.noise in ("numpy", "numpy_host")
         if self.kind == "dit":
             _lib.call("sf_dit_stream_reset", self.ctl.data_ptr(), self.S, self.n, self.D, self.x_ring.data_ptr(),
                       self.noise_dev.data_ptr() if use_host else None, self.noise_seed, st)
@@ -230,7 +267,7 @@ class StreamBatch:
         if self.done():
             raise StateError("stream batch already drained all generations")
         j, n, m, st = self.j, self.n, self.m, self._stream()
-        admit_next = self._fill_noise(j + 1) if self.noise == "numpy" else (j + 1 < m)
+        admit_next = self._fill_noise(j + 1) if self.noise in ("numpy", "numpy_host") else (j + 1 < m)
         if self.kind == "dit":
             _lib.call("sf_dit_stream_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, n, m,
                       self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
