@@ -275,6 +275,36 @@ int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t ge
  * fp32 cast (SF_F32, pipeline.py:176).  gen >= 0. */
 int sf_numpy_normal(const int64_t* seeds, int64_t gen, int64_t S, int64_t D, void* out, int out_dtype, void* stream);
 
+/* ---- Tiny-VAE (TAESD) decoder of retired frames (replaces decode_stub,
+ * src/pipeline.py:86-89).  Activations: bf16 NHWC, 64 channels, one-pixel zero
+ * border, [F][H+2][W+2][64]; buffers must be zero-initialised once (borders are
+ * never written). */
+typedef struct sf_taesd_weights {
+  const float* first_w; /* conv(4, 64): fp32 [64][4][3][3] (torch layout) */
+  const float* first_b; /* [64] */
+  const void* conv_w[33]; /* the 33 conv(64, 64) in network order: bf16 [9 taps][64 oc][64 ic] */
+  const float* conv_b[33]; /* [64] fp32, NULL for the three bias-free post-upsample convs */
+  const void* final_w;  /* conv(64, 3): bf16 [9][16][64], output channels 3..15 zero */
+  const float* final_b; /* [16] fp32 (3 used) */
+} sf_taesd_weights;
+
+/* Elements of one padded activation tensor. */
+int64_t sf_taesd_act_elems(int64_t F, int32_t H, int32_t W);
+/* 3x3 conv, 64 input channels, on padded NHWC bf16 (tcgen05 implicit GEMM).
+ * epi: 0 bias, 1 bias+ReLU, 2 bias+residual+ReLU (res: input geometry),
+ *      3 = 2 then 2x nearest upsample into out ([F][2H+2][2W+2][64]),
+ *      4 final: w [9][16][64], out fp32 NCHW image [F][3][H][W]. */
+int sf_conv3x3(const void* in, const void* w, const float* bias, const void* res, void* out, int64_t F, int32_t H,
+               int32_t W, int32_t epi, void* stream);
+/* Clamp(tanh(x/3)*3) + conv(4, 64) + ReLU: latent fp32 [F][4][64][64] -> padded stage-0 activation. */
+int sf_taesd_first(const float* lat, const float* w, const float* b, void* out, int64_t F, void* stream);
+/* Workspace of sf_taesd_decode for up to F_cap frames (4 stages x 3 padded
+ * activations), zero-initialised once by the caller and reused across calls. */
+int64_t sf_taesd_workspace_bytes(int64_t F_cap);
+/* Whole decoder: latents fp32 [F][4][64][64] -> images fp32 [F][3][512][512], F <= F_cap. */
+int sf_taesd_decode(const sf_taesd_weights* w, const float* lat, int64_t F, int64_t F_cap, void* ws, int64_t ws_bytes,
+                    float* img, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
