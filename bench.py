@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--model", default="s2", choices=["s2", "xl2"],
                     help="s2: DiT-S/2 (configs[1]); xl2: DiT-XL/2 (configs[3], 8-slot batch = 2 streams x 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true", help="skip the separately timed TAESD decode line")
     return ap.parse_args()
 
 
@@ -267,6 +268,23 @@ def main():
     e2e_ms, _ = timed(e2e_step, args.steps)
     e2e_value = frames / (e2e_ms / 1e3)
 
+    # ---- TAESD decode of the S frames one step retires (separately timed)
+    decode = None
+    if not args.no_decode and cfg.dim == 16384:
+        dec = sf.TinyDecoder(seed=0, max_frames=S)
+        img = torch.empty(S, 3, 512, 512, device="cuda")
+        lat = sb.frames.view(S, 4, 64, 64)
+        for _ in range(3):
+            dec.decode(lat, img)
+        torch.cuda.synchronize()
+        dec_ms, _ = timed(lambda: dec.decode(lat, img), args.steps)
+        d = dec_ms / args.steps
+        decode = {"decoder": "taesd (random init, taesd_decoder.pth layout)", "frames_per_decode": S,
+                  "ms_per_decode": round(d, 4), "decode_frames_per_s": round(S / d * 1e3, 1),
+                  "tflops": round(sf.TinyDecoder.flops_per_frame() * S / d / 1e9, 1),
+                  "value_with_decode": round(frames / ((total_ms + dec_ms) / 1e3), 1)}
+        del dec
+
     # ---- per-kernel roofline from a profiled eager step (CUDA events per launch)
     sb.profile_step()
     prof = sb.profile_step()
@@ -340,6 +358,8 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
+        if decode:
+            line["decode"] = decode
         if gathered:
             line["gather"] = gathered
         print(json.dumps(line), flush=True)

@@ -42,7 +42,8 @@ template <int NW>
 struct Cfg {
   static constexpr int W_BYTES = 9 * NW * 128;
   static constexpr int TMEM_COLS = ACC * NW < 32 ? 32 : ACC * NW;
-  static constexpr int SMEM = 1024 + W_BYTES + STAGES * STAGE_BYTES + 512 + NW * 4;
+  static constexpr int STG_BYTES = EPI_WARPS * 32 * 144;  // per-warp 32-pixel staging, 144 B pitch
+  static constexpr int SMEM = 1024 + W_BYTES + STAGES * STAGE_BYTES + 1024 + STG_BYTES;
 };
 
 struct ConvArgs {
@@ -53,8 +54,8 @@ struct ConvArgs {
   int tiles_per_frame;
 };
 
-__device__ __forceinline__ uint4 relu_add_pack(const float* v, const float* b, const uint4* r, int j, bool has_res,
-                                               bool relu) {
+__device__ __forceinline__ uint4 relu_add_pack(const float* v, const float* b, const uint4 (&r)[8], int j,
+                                               bool has_res, bool relu) {
   float x[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) x[i] = v[8 * j + i] + b[8 * j + i];
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* wbar = tempty + ACC;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
   float* sBias = reinterpret_cast<float*>(bars + 64);
+  uint8_t* sStage = reinterpret_cast<uint8_t*>(bars + 128);
 
   const uint32_t warp = warp_id(), lane = threadIdx.x & 31;
   const int Wp = a.W + 2;
@@ -184,39 +186,71 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
 
-      const int qf = Wp + tt * BM + quarter * 32 + lane;  // flat padded pixel within the frame
+      const int qf0 = Wp + tt * BM + quarter * 32;  // flat padded pixel of lane 0 within the frame
+      const int qf = qf0 + lane;
       const int y = qf / Wp, x = qf - y * Wp;
-      if (y > a.H || x < 1 || x > a.W) continue;  // border / beyond the last row: never written
-      const int64_t gp = (int64_t)f * P + qf;
+      const bool valid = y <= a.H && x >= 1 && x <= a.W;  // borders / beyond the last row: never written
       if constexpr (EPI == EPI_FINAL) {
-        float* img = reinterpret_cast<float*>(a.out) + (int64_t)f * 3 * a.H * a.W + (int64_t)(y - 1) * a.W + (x - 1);
+        if (valid) {
+          float* img = reinterpret_cast<float*>(a.out) + (int64_t)f * 3 * a.H * a.W + (int64_t)(y - 1) * a.W + (x - 1);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) img[(int64_t)c * a.H * a.W] = v[c] + sBias[c];
+          for (int c = 0; c < 3; ++c) img[(int64_t)c * a.H * a.W] = v[c] + sBias[c];
+        }
       } else {
+        // The warp moves its 32 pixels (128 B each) through smem so that global loads /
+        // stores are whole 128-byte lines (8 lanes per pixel) instead of 32 lines per
+        // instruction.
         constexpr bool RES = EPI == EPI_RES_RELU || EPI == EPI_RES_RELU_UP2;
         constexpr bool RELU = EPI != EPI_NONE;
-        const uint4* r = RES ? reinterpret_cast<const uint4*>(a.res + gp * CH) : nullptr;
-        uint4 o[8];
+        uint8_t* stg = sStage + quarter * (32 * 144);
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        const int64_t gp0 = (int64_t)f * P + qf0;
+        uint4 rr[8];
+        if constexpr (RES) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = relu_add_pack(v, sBias, r, j, RES, RELU);
+          for (int i = 0; i < 8; ++i) {
+            const int p = 4 * i + (lane >> 3), c = lane & 7;
+            uint4 val = make_uint4(0u, 0u, 0u, 0u);
+            if ((vmask >> p) & 1) val = reinterpret_cast<const uint4*>(a.res + (gp0 + p) * CH)[c];
+            *reinterpret_cast<uint4*>(stg + p * 144 + c * 16) = val;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rr[j] = *reinterpret_cast<const uint4*>(stg + lane * 144 + j * 16);
+          __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(stg + lane * 144 + j * 16) = relu_add_pack(v, sBias, rr, j, RES, RELU);
+        __syncwarp();
+        __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.out);
         if constexpr (EPI == EPI_RES_RELU_UP2) {
+          // pixel (y, x) -> (2y-1, 2x-1), (2y-1, 2x), (2y, 2x-1), (2y, 2x) of the next stage:
+          // 256 contiguous bytes in each of two rows; 2 pixels per instruction per row
           const int Wp2 = 2 * a.W + 2;
           const int64_t P2 = (int64_t)(2 * a.H + 2) * Wp2;
-          __nv_bfloat16* o2 = reinterpret_cast<__nv_bfloat16*>(a.out);
+#pragma unroll 4
+          for (int i = 0; i < 16; ++i) {
+            const int p = 2 * i + (lane >> 4), c = lane & 15;
+            const int yp = __shfl_sync(0xffffffffu, y, p), xp = __shfl_sync(0xffffffffu, x, p);
+            if ((vmask >> p) & 1) {
+              const uint4 val = *reinterpret_cast<const uint4*>(stg + p * 144 + (c & 7) * 16);
 #pragma unroll
-          for (int ry = 0; ry < 2; ++ry) {
-            uint4* d = reinterpret_cast<uint4*>(o2 + ((int64_t)f * P2 + (int64_t)(2 * y - 1 + ry) * Wp2 + 2 * x - 1) * CH);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              d[j] = o[j];
-              d[8 + j] = o[j];
+              for (int ry = 0; ry < 2; ++ry)
+                reinterpret_cast<uint4*>(outp + ((int64_t)f * P2 + (int64_t)(2 * yp - 1 + ry) * Wp2 + 2 * xp - 1) * CH)[c] =
+                    val;
             }
           }
         } else {
-          uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + gp * CH);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) d[j] = o[j];
+          for (int i = 0; i < 8; ++i) {
+            const int p = 4 * i + (lane >> 3), c = lane & 7;
+            if ((vmask >> p) & 1)
+              reinterpret_cast<uint4*>(outp + (gp0 + p) * CH)[c] =
+                  *reinterpret_cast<const uint4*>(stg + p * 144 + c * 16);
+          }
         }
+        __syncwarp();  // staging is rewritten by the next tile
       }
     }
   }

@@ -53,7 +53,11 @@ class PipelineState:
 
 @dataclass(frozen=True)
 class DecodedPayload:
+    """decode_stub's payload (pipeline.py:53-56); ``image`` is set when a device
+    decoder (vae.TinyDecoder) decoded the frame: [3, 512, 512] fp32."""
+
     latent: np.ndarray
+    image: np.ndarray | None = None
 
 
 @dataclass(frozen=True)
@@ -154,7 +158,8 @@ class StreamBatch:
 
     def __init__(self, model: VelocityModel, sched: TimeWindowSchedule, n: int, num_streams: int = 1,
                  cond: Conditioning | list | None = None, seed: int | list = 0, m: int | None = None,
-                 dtype=np.float64, noise: str = "numpy", use_graph: bool = True, device: str = "cuda"):
+                 dtype=np.float64, noise: str = "numpy", use_graph: bool = True, device: str = "cuda",
+                 decoder=None):
         if not torch.cuda.is_available():
             raise RuntimeError("StreamBatch needs a CUDA device; there is no CPU fallback")
         _check_run_args(1 if m is None else m, n, sched)
@@ -214,6 +219,12 @@ class StreamBatch:
             if any(int(v) >= 1 << 63 for v in self.seeds):
                 raise ParameterError("seeds must be < 2**63 for the device generator")
             self.seeds_dev = torch.tensor([int(v) for v in self.seeds], dtype=torch.int64, device=dev)
+        self.decoder = decoder
+        self.images = None
+        if decoder is not None:
+            if self.D != 16384 or decoder.max_frames < self.S:
+                raise ParameterError("the TAESD decoder takes 4x64x64 latents, one per stream (max_frames >= S)")
+            self.images = torch.zeros(self.S, 3, 512, 512, dtype=torch.float32, device=dev)
         self._h2d_done = torch.cuda.Event()
         self.stats = [RunStats() for _ in range(self.S)]
         self.j = 0
@@ -303,6 +314,9 @@ class StreamBatch:
         if 0 <= retiring < m:
             for rs in self.stats:
                 rs.decodes += 1
+            if self.decoder is not None:  # decode the retired frames on the same stream
+                lat = self.frames if self.frames.dtype == torch.float32 else self.frames.float()
+                self.decoder.decode(lat.view(self.S, 4, 64, 64), self.images)
             return retiring
         return -1
 
@@ -381,12 +395,15 @@ class StreamBatch:
         if g < 0:
             return []
         frames = self.frames.cpu().numpy()
+        images = self.images.cpu().numpy() if self.decoder is not None else None
         out = []
         for s in range(self.S):
             lat = frames[s].copy()
             self.stats[s].decode_time_us += decode_cost_us
-            out.append((s, GenerationResult(id=g, latent=lat, decoded=decode_stub(lat, decode_cost_us),
-                                            iterations_spanned=self.n)))
+            dec = decode_stub(lat, decode_cost_us)
+            if images is not None:
+                dec = DecodedPayload(latent=dec.latent, image=images[s].copy())
+            out.append((s, GenerationResult(id=g, latent=lat, decoded=dec, iterations_spanned=self.n)))
         return out
 
     def __call__(self, m: int | None = None) -> list:
@@ -422,13 +439,15 @@ class StreamBatch:
 # ----------------------------------------------------------------------------- reference entry points
 def run_stream(m: int, n: int, model: VelocityModel, cond: Conditioning, seed: int, sched: TimeWindowSchedule,
                sched_cost_us: float = 0.0, decode_cost_us: float = 0.0, dtype=np.float64,
-               on_iteration: Callable[[PipelineState], None] | None = None):
+               on_iteration: Callable[[PipelineState], None] | None = None, decoder=None):
     """pipeline.py:139-220: m generations of n steps in m+n-1 iterations,
-    through the device-resident stream batch (one stream)."""
+    through the device-resident stream batch (one stream).  ``decoder`` (an
+    extension: vae.TinyDecoder) decodes each retired frame on the device."""
     _check_run_args(m, n, sched)
     if isinstance(model, DiTVelocityModel) and np.dtype(dtype) == np.float64:
         dtype = np.float32  # the DiT ring is fp32 (documented in DESIGN.md)
-    sb = StreamBatch(model, sched, n, num_streams=1, cond=cond, seed=seed, m=m, dtype=dtype, noise="numpy")
+    sb = StreamBatch(model, sched, n, num_streams=1, cond=cond, seed=seed, m=m, dtype=dtype, noise="numpy",
+                     decoder=decoder)
     results = []
     while not sb.done():
         busy_wait_us(sched_cost_us)

@@ -104,3 +104,24 @@ def test_decoder_frame_independence_and_reuse():
     assert torch.equal(full[2:3], one)
     again = dec.decode(lat)
     assert torch.equal(full, again)
+
+
+def test_stream_batch_decodes_retired_frames():
+    """StreamBatch(decoder=...) returns each retired frame's image = decode(latent)."""
+    import numpy as np
+
+    import paper_2511_22009_b200 as sf
+
+    sched = sf.build_time_window_schedule(inference_steps=2)
+    model = sf.SeededMockModel(dim=16384, seed=4)
+    cond = sf.make_conditioning(np.zeros(8))
+    dec = V.TinyDecoder(seed=2, max_frames=2)
+    sb = sf.StreamBatch(model, sched, 2, num_streams=2, cond=cond, seed=[1, 2], m=2, dtype=np.float32, decoder=dec)
+    got = []
+    while not sb.done():
+        got += sb.step()
+    assert [r.id for _, r in got] == [0, 0, 1, 1]
+    for _, r in got:
+        want = dec.decode(torch.from_numpy(r.latent).cuda().view(1, 4, 64, 64)).cpu().numpy()[0]
+        assert r.decoded.image.shape == (3, 512, 512)
+        assert np.array_equal(r.decoded.image, want)
