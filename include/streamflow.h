@@ -174,6 +174,13 @@ int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float
 int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, void* xmod, const float* gate,
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream);
+/* Fused DiT-S/2 MLP block (hidden 384, MLP 1536): xres += gate * (GELU(xmod W1^T + b1) W2^T + b2);
+ * xmod = LN(xres) * (1 + scale) + shift -- the hidden never leaves the SM.  xmod is read
+ * (this block's modulated input) and overwritten (the next LayerNorm's output).
+ * M and tokens_per_slot multiples of 128. */
+int sf_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const float* b1, const float* b2, void* xres,
+                 void* xmod_out, const float* gate, const float* shift, const float* scale, int64_t vec_stride,
+                 float ln_eps, int64_t M, int32_t tokens_per_slot, void* stream);
 
 /* K6 -- flash attention, T tokens per row (multiple of 256), head dim 64, no mask.
  * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T] fp16;

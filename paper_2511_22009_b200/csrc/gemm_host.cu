@@ -92,10 +92,13 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
+#ifndef SF_QKV_WARPS
+#define SF_QKV_WARPS 4  // epilogue warps of the head-dim-64 QKV GEMM (4 or 12)
+#endif
 template <int BN, int KIND>
 constexpr int epi_warps() {
   // QKV: 4; RES_LN: 12; bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
-  return KIND == EPI_QKV ? 4 : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+  return KIND == EPI_QKV ? (BN == 192 ? SF_QKV_WARPS : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
 }
 
 // Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).

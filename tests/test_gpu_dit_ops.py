@@ -106,3 +106,45 @@ def test_attention_hd72_matches_sdpa(rows, H, scale):
     ref = ref.permute(0, 2, 1, 3).reshape(rows * T, H * hd)
     err = (out.float() - ref).abs().max().item()
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("rows", [1, 2, 3])
+def test_mlp_fused_matches_unfused(rows):
+    """sf_mlp_fused (fc1+GELU+fc2+gated residual+LN+modulate, hidden on chip) vs torch fp32
+    of the same block with the hidden rounded to bf16 (as the unfused path stores it), and
+    vs the unfused GEMM pair (sf_gemm_bf16 GELU -> sf_gemm_res_ln)."""
+    T, N, F = 1024, 384, 1536
+    M = rows * T
+    g = torch.Generator(device="cuda").manual_seed(40 + rows)
+    x = bf(torch.randn(M, N, device="cuda", generator=g))
+    w1 = bf(torch.randn(F, N, device="cuda", generator=g) * 0.05)
+    b1 = torch.randn(F, device="cuda", generator=g) * 0.1
+    w2 = bf(torch.randn(N, F, device="cuda", generator=g) * 0.03)
+    b2 = torch.randn(N, device="cuda", generator=g) * 0.1
+    xres0 = bf(torch.randn(M, N, device="cuda", generator=g))
+    vec_stride = 4 * N
+    vecs = torch.randn(rows, vec_stride, device="cuda", generator=g) * 0.5
+    gate, shift, scale = vecs[:, 0:N], vecs[:, N:2 * N], vecs[:, 2 * N:3 * N]
+    # fused (xmod in place, as the runtime uses it)
+    xres = xres0.clone()
+    xmod = x.clone()
+    L().call("sf_mlp_fused", xmod.data_ptr(), w1.data_ptr(), w2.data_ptr(), b1.data_ptr(), b2.data_ptr(),
+             xres.data_ptr(), xmod.data_ptr(), gate.data_ptr(), shift.data_ptr(), scale.data_ptr(), vec_stride,
+             1e-6, M, T, st())
+    # unfused pair
+    h = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_gemm_bf16", x.data_ptr(), w1.data_ptr(), b1.data_ptr(), h.data_ptr(), M, F, N, 2, st())
+    xres_u = xres0.clone()
+    xmod_u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_gemm_res_ln", h.data_ptr(), w2.data_ptr(), b2.data_ptr(), xres_u.data_ptr(), xmod_u.data_ptr(),
+             gate.data_ptr(), shift.data_ptr(), scale.data_ptr(), vec_stride, M, N, F, T, 1e-6, st())
+    torch.cuda.synchronize()
+    slot = torch.arange(M, device="cuda") // T
+    hh = torch.nn.functional.gelu(x.float() @ w1.float().t() + b1, approximate="tanh").to(torch.bfloat16).float()
+    y = xres0.float() + gate[slot] * (hh @ w2.float().t() + b2)
+    ref = torch.nn.functional.layer_norm(y, (N,), eps=1e-6) * (1 + scale[slot]) + shift[slot]
+    for got_r, got_m in ((xres, xmod), (xres_u, xmod_u)):
+        assert (got_r.float() - y).abs().max().item() < 3e-2 * max(1.0, y.abs().max().item())
+        assert (got_m.float() - ref).abs().max().item() < 5e-2 * max(1.0, ref.abs().max().item())
+    # fused and unfused agree to bf16 rounding of the same hidden
+    assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, y.abs().max().item())
