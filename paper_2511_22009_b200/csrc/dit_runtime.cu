@@ -542,7 +542,17 @@ static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[1
 }
 
 // Kernel classes for per-launch profiling (sf_dit_profile_step).
-enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_NCLS };
+// Fused MLP block for the DiT-S/2 geometry (sf_diag_mlp_fused(0) restores the fc1 / fc2 GEMM pair).
+static int g_mlp_fused = -1;  // -1: from the environment (SF_MLP_FUSED=0 disables), default on
+static bool mlp_fused_ok(const sf_dit_config& c) {
+  if (g_mlp_fused < 0) {
+    const char* e = getenv("SF_MLP_FUSED");
+    g_mlp_fused = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_mlp_fused && c.hidden == 384 && c.mlp_hidden == 1536;
+}
+
+enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_MLP, P_NCLS };
 
 // Called after every launch: counts launches and, in a profiled step, records
 // a CUDA event so each launch's duration can be attributed to its class.
@@ -599,6 +609,17 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
     mark(h, P_ATTN, st);
     for (int half = 0; half < 2; ++half) {  // 0: attention proj (gate_msa), 1: MLP (fc1 + GELU, fc2, gate_mlp)
+      if (half == 1 && mlp_fused_ok(c)) {
+        // DiT-S/2: the whole MLP block in one kernel (hidden kept on chip, csrc/mlp_fused.cu)
+        const float* nxt = l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6;
+        if ((rc = launch_mlp_fused(h->xmod, (const __nv_bfloat16*)h->w.fc1_w + (int64_t)l * c.mlp_hidden * H,
+                                   (const __nv_bfloat16*)h->w.fc2_w + (int64_t)l * H * c.mlp_hidden,
+                                   h->w.fc1_b + (int64_t)l * c.mlp_hidden, h->w.fc2_b + (int64_t)l * H, h->xres,
+                                   h->xmod, h->mod + l * B6 + 5 * H, nxt, nxt + H, h->mod_stride, c.ln_eps, M, T, st)))
+          return rc;
+        mark(h, P_MLP, st);
+        continue;
+      }
       if (half == 1) {
         EpiParams ep{};
         ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
@@ -907,6 +928,8 @@ int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t ge
   philox_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out, S, D, seed, gen);
   return cuda_status();
 }
+
+void sf_diag_mlp_fused(int on) { g_mlp_fused = on; }
 
 int sf_dit_mod_stride(const sf_dit_config* c) { return c->depth * 6 * c->hidden + 2 * c->hidden; }
 

@@ -51,8 +51,11 @@ constexpr int H_BYTES = BM * HC * 2;  // 16 KB
 #ifndef SF_MLP_GELU_WARPS
 #define SF_MLP_GELU_WARPS 8
 #endif
+#ifndef SF_MLP_PF
+#define SF_MLP_PF -1  // hidden chunk at which the boundary's residual / next X are prefetched to L2 (-1: off)
+#endif
 #ifndef SF_MLP_CL
-#define SF_MLP_CL 2  // CTAs per cluster sharing (TMA-multicasting) the weight stream
+#define SF_MLP_CL 1  // CTAs per cluster sharing (TMA-multicasting) the weight stream
 #endif
 constexpr int CL = SF_MLP_CL;
 constexpr uint16_t CL_MASK = (1u << CL) - 1;
@@ -74,6 +77,12 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, 
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
+}
+// L2 prefetch of one TMA box (no smem, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 // Arrive on the same-offset mbarrier of every CTA in `mask` once this thread's prior MMAs complete.
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
@@ -198,6 +207,14 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmX, xfull, kb * 64, tile * BM);
         w1(1);
         for (int c = 0; c < NCH; ++c) {
+          if (SF_MLP_PF >= 0 && c == SF_MLP_PF) {
+            // L2 prefetch of what the tile boundary waits on: this tile's residual rows and
+            // the next tile's X (the X buffer is reloaded twice per tile, serially)
+            for (int kb = 0; kb < 6; ++kb) {
+              tma_prefetch_2d(&tmR, kb * 64, tile * BM);
+              if (tile + tstride < tiles) tma_prefetch_2d(&tmX, kb * 64, (tile + tstride) * BM);
+            }
+          }
           w2(c);
           if (c + 2 < NCH) w1(c + 2);
           if (c == NCH - 2) {  // all fc1 of this tile issued: residual rows replace X when it is consumed

@@ -37,5 +37,9 @@ int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, in
                    int hd);
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st);
 
+int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const float* b1, const float* b2,
+                     __nv_bfloat16* xres, __nv_bfloat16* xmod_out, const float* gate, const float* shift,
+                     const float* scale, int64_t vec_stride, float ln_eps, int64_t M, int T, cudaStream_t st);
+
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
 }  // namespace sf
