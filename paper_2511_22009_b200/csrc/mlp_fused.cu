@@ -31,7 +31,7 @@ namespace mlp {
 #define SF_MLP_TRACE 0
 #endif
 #if SF_MLP_TRACE
-__device__ long long g_mlp_trace[8 * 64];
+__device__ long long g_mlp_trace[16 * 64];
 #define MTR(role, idx)                                                              \
   do {                                                                              \
     if (blockIdx.x == 0 && (idx) < 64) g_mlp_trace[(role) * 64 + (idx)] = clock64(); \
@@ -54,16 +54,21 @@ constexpr int H_BYTES = BM * HC * 2;  // 16 KB
 #ifndef SF_MLP_PF
 #define SF_MLP_PF -1  // hidden chunk at which the boundary's residual / next X are prefetched to L2 (-1: off)
 #endif
+#ifndef SF_MLP_PFX
+#define SF_MLP_PFX -1  // hidden chunk at which the next tile's X is prefetched to L2 (-1: off)
+#endif
 #ifndef SF_MLP_CL
 #define SF_MLP_CL 1  // CTAs per cluster sharing (TMA-multicasting) the weight stream
 #endif
 constexpr int CL = SF_MLP_CL;
 constexpr uint16_t CL_MASK = (1u << CL) - 1;
 #ifndef SF_MLP_EPI_WARPS
-#define SF_MLP_EPI_WARPS 8
+#define SF_MLP_EPI_WARPS 8  // dedicated epilogue warps (the GELU warps join them per tile)
 #endif
 constexpr int GELU_WARPS = SF_MLP_GELU_WARPS, EPI_WARPS = SF_MLP_EPI_WARPS;
-constexpr int ECOLS = D / (EPI_WARPS / 4);  // output columns per epilogue thread
+constexpr int WORKERS = GELU_WARPS + EPI_WARPS;  // warps sharing the epilogue
+constexpr int PARTS = WORKERS / 4;                // per TMEM lane quarter
+constexpr int ECOLS = D / PARTS;                  // output columns per epilogue thread
 constexpr int GCOLS = HC / (GELU_WARPS / 4);  // hidden columns per GELU thread
 constexpr int THREADS = 32 * (2 + GELU_WARPS + EPI_WARPS);
 constexpr int ACC2 = 0, ACC1 = 384;
@@ -158,9 +163,9 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       mbar_init(&hempty[b], 1);
     }
     mbar_init(a2full, 1);
-    mbar_init(a2empty, EPI_WARPS * 32);
+    mbar_init(a2empty, WORKERS * 32);
     mbar_init(rfull, 1);
-    mbar_init(xfree, EPI_WARPS * 32);
+    mbar_init(xfree, WORKERS * 32);
     fence_barrier_init();
   }
   for (int i = threadIdx.x; i < FF; i += THREADS) sB1[i] = p.b1[i];
@@ -203,22 +208,22 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         // the X buffer: X(tile) for fc1, then the tile's residual rows for the epilogue
         w1(0);
         mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's epilogue left the buffer
+        MTR(8, local);
         mbar_expect_tx(xfull, X_BYTES);
         for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmX, xfull, kb * 64, tile * BM);
         w1(1);
         for (int c = 0; c < NCH; ++c) {
-          if (SF_MLP_PF >= 0 && c == SF_MLP_PF) {
-            // L2 prefetch of what the tile boundary waits on: this tile's residual rows and
-            // the next tile's X (the X buffer is reloaded twice per tile, serially)
-            for (int kb = 0; kb < 6; ++kb) {
-              tma_prefetch_2d(&tmR, kb * 64, tile * BM);
-              if (tile + tstride < tiles) tma_prefetch_2d(&tmX, kb * 64, (tile + tstride) * BM);
-            }
-          }
+          // L2 prefetch of what the tile boundary waits on: this tile's residual rows and
+          // the next tile's X (the X buffer is reloaded twice per tile, serially)
+          if (SF_MLP_PF >= 0 && c == SF_MLP_PF)
+            for (int kb = 0; kb < 6; ++kb) tma_prefetch_2d(&tmR, kb * 64, tile * BM);
+          if (SF_MLP_PFX >= 0 && c == SF_MLP_PFX && tile + tstride < tiles)
+            for (int kb = 0; kb < 6; ++kb) tma_prefetch_2d(&tmX, kb * 64, (tile + tstride) * BM);
           w2(c);
           if (c + 2 < NCH) w1(c + 2);
           if (c == NCH - 2) {  // all fc1 of this tile issued: residual rows replace X when it is consumed
             mbar_wait(xempty, local & 1);
+            MTR(9, local);
             mbar_expect_tx(rfull, X_BYTES);
             for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmR, rfull, kb * 64, tile * BM);
           }
@@ -312,90 +317,106 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         if (c + 2 < NCH) fc1(c + 2);
       }
     }
-  } else if (warp < 2 + GELU_WARPS) {
-    // ------------------------------------------------------------ GELU warps
-    const uint32_t quarter = warp & 3, part = (warp - 2) >> 2;  // part: which GCOLS columns of the chunk
-    const uint32_t row = quarter * 32 + lane;
-    const uint32_t taddr = tmem + ((quarter * 32) << 16) + ACC1 + part * GCOLS;
-    int g = 0;
-    for (int tile = tile0; tile < tiles; tile += tstride) {
-      for (int c = 0; c < NCH; ++c, ++g) {
-        const int b = g & 1;
-        mbar_wait(&a1full[b], (g >> 1) & 1);
-        if (warp == 2 && lane == 0) MTR(4, g);
-        tc_fence_after();
-        // 32 columns at a time (register budget); the TMEM buffer is released after the last read
-        const float* bb = sB1 + c * HC + part * GCOLS;
-        uint32_t pk[GCOLS / 2];
-#pragma unroll
-        for (int h = 0; h < GCOLS / 32; ++h) {
-          float v[32];
-          tmem_ld32(taddr + 64 * b + 32 * h, v);
-          tmem_ld_wait();
-          if (h + 1 == GCOLS / 32) {
-            tc_fence_before();
-            mbar_arrive(&a1empty[b]);
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 bv = reinterpret_cast<const float2*>(bb + 32 * h)[i];
-            float2 y = __fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), bv);
-            y = gelu_tanh2(y);
-            pk[16 * h + i] = pack_bf16(y.x, y.y);
-          }
-        }
-        mbar_wait(&hempty[b], ((g >> 1) & 1) ^ 1);  // fc2 read this buffer two chunks ago
-        uint8_t* hrow = sH + b * H_BYTES + row * 128;
-#pragma unroll
-        for (int j = 0; j < GCOLS / 8; ++j) {
-          const int cj = part * (GCOLS / 8) + j;  // 16-byte chunk of the 128-byte row
-          *reinterpret_cast<uint4*>(hrow + ((cj ^ (row & 7)) * 16)) =
-              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&hfull[b]);
-        if (warp == 2 && lane == 0) MTR(5, g);
-      }
-    }
   } else {
-    // ------------------------------------------------------------ residual + LayerNorm epilogue
-    // EPI_WARPS / 4 warps per TMEM lane quarter, ECOLS columns each.  The tile's residual
-    // rows arrive by TMA in the X buffer (free once fc1 is done); the updated residual
-    // and then the modulated LayerNorm output are written back in place and leave by
-    // TMA stores (32-row slices per warp), so global traffic is bulk, not per thread.
-    const uint32_t e = warp - 2 - GELU_WARPS;
-    const uint32_t quarter = warp & 3, part = e >> 2;
+    // ------------------------------------------------------------ worker warps 2..17
+    // Warps 2..(1+GELU_WARPS) run the GELU of every hidden chunk; after a tile's last
+    // chunk they join the dedicated epilogue warps, so all WORKERS warps share the
+    // residual + LayerNorm epilogue (the MMA pipe waits on it at the tile boundary).
+    const bool is_gelu = warp < 2 + GELU_WARPS;
+    const uint32_t quarter = warp & 3;
     const uint32_t row = quarter * 32 + lane;
+    const uint32_t gpart = (warp - 2) >> 2;  // GELU: which GCOLS columns of a chunk
+    const uint32_t gaddr = tmem + ((quarter * 32) << 16) + ACC1 + gpart * GCOLS;
+    const uint32_t e = warp - 2;              // epilogue: 0..WORKERS-1
+    const uint32_t part = e >> 2;             // ECOLS-column slice of the row
     const int col0 = ECOLS * part;
-    const uint32_t taddr = tmem + ((quarter * 32) << 16) + ACC2 + col0;
+    const uint32_t eaddr = tmem + ((quarter * 32) << 16) + ACC2 + col0;
     constexpr int NQ = ECOLS / 32;
-    constexpr int PARTS = EPI_WARPS / 4;
     // 16-byte chunk j (8 columns) of this thread's row within 64-column atom a
     auto xp = [&](int col) -> uint4* {
       const int a = col >> 6, j = (col & 63) >> 3;
       return reinterpret_cast<uint4*>(sX + a * X_ATOM + row * 128 + ((j ^ (row & 7)) * 16));
     };
-    int local = 0;
+    // TMA-store the quarter's 32 rows of the X buffer (6 atoms; warp k of the quarter
+    // issues atoms k, k + 4) once every warp of the quarter has written its columns
+    auto store_quarter = [&](const CUtensorMap* m, int r0) {
+      fence_proxy_async_smem();
+      named_bar_sync(2 + quarter, 32 * PARTS);
+      if (lane == 0) {
+        for (int a = (int)part; a < 6; a += PARTS)
+          tma_store_2d(m, sX + a * X_ATOM + quarter * 32 * 128, 64 * a, r0 + quarter * 32);
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+      __syncwarp();
+      named_bar_sync(2 + quarter, 32 * PARTS);  // the stores have read the quarter's rows
+    };
+    int g = 0, local = 0;
     for (int tile = tile0; tile < tiles; tile += tstride, ++local) {
+      if (is_gelu) {
+        for (int c = 0; c < NCH; ++c, ++g) {
+          const int b = g & 1;
+          mbar_wait(&a1full[b], (g >> 1) & 1);
+          if (warp == 2 && lane == 0) MTR(4, g);
+          tc_fence_after();
+          // 32 columns at a time (register budget); the TMEM buffer is released after the last read
+          const float* bb = sB1 + c * HC + gpart * GCOLS;
+          uint32_t pk[GCOLS / 2];
+#pragma unroll
+          for (int h = 0; h < GCOLS / 32; ++h) {
+            float v[32];
+            tmem_ld32(gaddr + 64 * b + 32 * h, v);
+            tmem_ld_wait();
+            if (h + 1 == GCOLS / 32) {
+              tc_fence_before();
+              mbar_arrive(&a1empty[b]);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float2 bv = reinterpret_cast<const float2*>(bb + 32 * h)[i];
+              float2 y = __fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), bv);
+              y = gelu_tanh2(y);
+              pk[16 * h + i] = pack_bf16(y.x, y.y);
+            }
+          }
+          mbar_wait(&hempty[b], ((g >> 1) & 1) ^ 1);  // fc2 read this buffer two chunks ago
+          uint8_t* hrow = sH + b * H_BYTES + row * 128;
+#pragma unroll
+          for (int j = 0; j < GCOLS / 8; ++j) {
+            const int cj = gpart * (GCOLS / 8) + j;  // 16-byte chunk of the 128-byte row
+            *reinterpret_cast<uint4*>(hrow + ((cj ^ (row & 7)) * 16)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&hfull[b]);
+          if (warp == 2 && lane == 0) MTR(5, g);
+        }
+      }
+      // ---------------- residual + LayerNorm epilogue of this tile (all workers)
+      // The tile's residual rows arrive by TMA in the X buffer (free once fc1 is done);
+      // the updated residual and then the modulated LayerNorm output are written back in
+      // place and leave by TMA stores, so global traffic is bulk, not per thread.
       const int r0 = tile * BM;
       const int64_t slot = r0 / p.T;
-      named_bar_sync(1, EPI_WARPS * 32);  // previous tile's readers are done with sVec
-      for (int i = e * 32 + lane; i < D; i += EPI_WARPS * 32) {
+      named_bar_sync(1, WORKERS * 32);  // previous tile's readers are done with sVec
+      for (int i = e * 32 + lane; i < D; i += WORKERS * 32) {
         const int64_t o = slot * p.vec_stride + i;
         sVec[i] = p.b2[i];
         sVec[D + i] = p.gate[o];
         sVec[2 * D + i] = p.shift[o];
         sVec[3 * D + i] = p.scale[o];
       }
-      named_bar_sync(1, EPI_WARPS * 32);
+      named_bar_sync(1, WORKERS * 32);
       mbar_wait(a2full, local & 1);
+      if (e == 0 && lane == 0) MTR(10, local);
       mbar_wait(rfull, local & 1);
+      if (e == 0 && lane == 0) MTR(11, local);
       tc_fence_after();
       float sum = 0.f, sq = 0.f;
-#pragma unroll 1
+#pragma unroll
       for (int q = 0; q < NQ; ++q) {
         float v[32];
-        tmem_ld32(taddr + 32 * q, v);
+        tmem_ld32(eaddr + 32 * q, v);
         tmem_ld_wait();
         if (q + 1 == NQ) {
           tc_fence_before();
@@ -421,31 +442,21 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
           *ptr = make_uint4(nw[0], nw[1], nw[2], nw[3]);
         }
       }
-      // updated residual out: this warp's 32 rows x ECOLS columns
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        for (int a = 0; a < ECOLS / 64; ++a)
-          tma_store_2d(&tmRs, sX + (col0 / 64 + a) * X_ATOM + quarter * 32 * 128, col0 + 64 * a, r0 + quarter * 32);
-        bulk_commit();
-      }
       // row statistics over the column parts of this lane quarter
       sRed[(0 * PARTS + part) * BM + row] = sum;
       sRed[(1 * PARTS + part) * BM + row] = sq;
-      named_bar_sync(2 + quarter, 32 * PARTS);
+      store_quarter(&tmRs, r0);  // updated residual out (its barriers also publish sRed)
       float tsum = 0.f, tsq = 0.f;
 #pragma unroll
       for (int k = 0; k < PARTS; ++k) {
         tsum += sRed[k * BM + row];
         tsq += sRed[(PARTS + k) * BM + row];
       }
-      named_bar_sync(2 + quarter, 32 * PARTS);  // all read before the next tile overwrites
       const float mean = tsum * (1.0f / D);
       const float var = fmaxf(tsq * (1.0f / D) - mean * mean, 0.f);
       const float rstd = rsqrtf(var + p.ln_eps);
-      if (lane == 0) bulk_wait_read<0>();  // the residual store has read the buffer
-      __syncwarp();
-#pragma unroll 1
+      if (e == 0 && lane == 0) MTR(12, local);
+#pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const float* vsh = sVec + 2 * D + col0 + 32 * q;
         const float* vsc = sVec + 3 * D + col0 + 32 * q;
@@ -465,19 +476,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
           *ptr = make_uint4(o[0], o[1], o[2], o[3]);
         }
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        for (int a = 0; a < ECOLS / 64; ++a)
-          tma_store_2d(&tmMs, sX + (col0 / 64 + a) * X_ATOM + quarter * 32 * 128, col0 + 64 * a, r0 + quarter * 32);
-        bulk_commit();
-        bulk_wait_read<0>();  // the buffer may be refilled with the next X
-      }
-      __syncwarp();
+      store_quarter(&tmMs, r0);  // modulated LayerNorm out; the X buffer is then free
+      if (e == 0 && lane == 0) MTR(13, local);
       mbar_arrive(xfree);
     }
-    if (lane == 0) bulk_wait<0>();
-    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -548,7 +550,7 @@ int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const 
 
 #if SF_MLP_TRACE
 extern "C" int sf_mlp_trace_read(long long* dst) {
-  return cudaMemcpyFromSymbol(dst, sf::mlp::g_mlp_trace, sizeof(long long) * 8 * 64) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(dst, sf::mlp::g_mlp_trace, sizeof(long long) * 16 * 64) == cudaSuccess ? 0 : -1;
 }
 #endif
 
