@@ -42,11 +42,15 @@ __device__ long long g_mlp_trace[16 * 64];
   } while (0)
 #endif
 
+#ifndef SF_MLP_PAIR
+#define SF_MLP_PAIR 0  // 2-CTA pairs (measured slower: 384 vs 315 us; cross-CTA GELU handoffs): cta_group::2 MMAs (M=256), the weight operand split between the SMs
+#endif
 constexpr int D = 384, FF = 1536, BM = 128, HC = 64, NCH = FF / HC;  // 24 hidden chunks
 constexpr int X_ATOM = BM * 64 * 2;                                   // 16 KB: 128 rows x 64 K
 constexpr int X_BYTES = 6 * X_ATOM;                                   // 96 KB
-constexpr int STAGE = 24576;                                          // 24 KB weight block
-constexpr int NSTAGE = 3;
+constexpr int WBLOCK = 24576;                                         // 24 KB weight block (both CTAs)
+constexpr int STAGE = WBLOCK / (SF_MLP_PAIR ? 2 : 1);                  // this CTA's share
+constexpr int NSTAGE = SF_MLP_PAIR ? 6 : 3;
 constexpr int H_BYTES = BM * HC * 2;  // 16 KB
 #ifndef SF_MLP_GELU_WARPS
 #define SF_MLP_GELU_WARPS 8
@@ -60,8 +64,11 @@ constexpr int H_BYTES = BM * HC * 2;  // 16 KB
 #ifndef SF_MLP_CL
 #define SF_MLP_CL 1  // CTAs per cluster sharing (TMA-multicasting) the weight stream
 #endif
-constexpr int CL = SF_MLP_CL;
+constexpr bool PAIR = SF_MLP_PAIR;
+constexpr int CL = PAIR ? 2 : SF_MLP_CL;
+static_assert(!PAIR || SF_MLP_CL == 1, "pair mode and weight multicast are exclusive");
 constexpr uint16_t CL_MASK = (1u << CL) - 1;
+constexpr int WSPLIT = PAIR ? 2 : 1;  // each CTA holds 1/WSPLIT of every weight block
 #ifndef SF_MLP_EPI_WARPS
 #define SF_MLP_EPI_WARPS 8  // dedicated epilogue warps (the GELU warps join them per tile)
 #endif
@@ -142,6 +149,9 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   const uint32_t warp = warp_id(), lane = threadIdx.x & 31;
   const int tiles = p.M / BM;
   const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  // barriers that collect arrivals from both CTAs of a pair live in the leader
+  auto lead = [&](uint64_t* bar) -> uint32_t { return mapa_shared(smem_u32(bar), 0); };
   // CTA `crank` of cluster k takes tiles (k + i * nclusters) * CL + crank: every CTA of a
   // cluster runs the same number of tiles (tiles % CL == 0), so their weight streams match
   const int tile0 = (blockIdx.x / CL) * CL + crank, tstride = gridDim.x;
@@ -152,24 +162,30 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
     tma_prefetch(&tmW2);
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&wfull[s], 1);
-      mbar_init(&wempty[s], CL);  // every CTA of the cluster must have consumed the slot
+      mbar_init(&wempty[s], PAIR ? 1 : CL);  // multicast: every CTA's MMAs must have consumed the slot
     }
     mbar_init(xfull, 1);
     mbar_init(xempty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a1full[b], 1);
-      mbar_init(&a1empty[b], GELU_WARPS * 32);
-      mbar_init(&hfull[b], GELU_WARPS * 32);
+      mbar_init(&a1empty[b], WSPLIT * GELU_WARPS * 32);
+      mbar_init(&hfull[b], WSPLIT * GELU_WARPS * 32);
       mbar_init(&hempty[b], 1);
     }
     mbar_init(a2full, 1);
-    mbar_init(a2empty, WORKERS * 32);
+    mbar_init(a2empty, WSPLIT * WORKERS * 32);
     mbar_init(rfull, 1);
     mbar_init(xfree, WORKERS * 32);
     fence_barrier_init();
   }
   for (int i = threadIdx.x; i < FF; i += THREADS) sB1[i] = p.b1[i];
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc_2sm<512>(tmem_holder);
+    else
+      tmem_alloc<512>(tmem_holder);
+  }
+  if constexpr (CL > 1) cluster_sync_all();  // the peer's barriers exist before any remote arrive
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -184,14 +200,24 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       auto wblock = [&](const CUtensorMap* m, int c0, int c1, int nload, int step_c0, int rows) {
         const int s = ws % NSTAGE;
         mbar_wait(&wempty[s], ((ws / NSTAGE) & 1) ^ 1);
-        mbar_expect_tx(&wfull[s], STAGE);
-        const int part = rows / CL;
-        for (int i = 0; i < nload; ++i) {
-          uint8_t* dst = sW + s * STAGE + i * (STAGE / nload) + crank * part * 128;
-          if constexpr (CL > 1)
-            tma_load_2d_mc(dst, m, &wfull[s], c0 + i * step_c0, c1 + crank * part, CL_MASK);
-          else
-            tma_load_2d(dst, m, &wfull[s], c0 + i * step_c0, c1);
+        if constexpr (PAIR) {
+          // this CTA's half of the block's rows (the pair MMA reads B from both CTAs);
+          // both halves complete on the leader's full barrier
+          const int part = rows / 2;
+          if (leader) mbar_expect_tx(&wfull[s], WBLOCK);
+          for (int i = 0; i < nload; ++i)
+            tma_load_2d_2sm(sW + s * STAGE + i * (STAGE / nload), m, lead(&wfull[s]), c0 + i * step_c0,
+                            c1 + crank * part);
+        } else {
+          mbar_expect_tx(&wfull[s], STAGE);
+          const int part = rows / CL;
+          for (int i = 0; i < nload; ++i) {
+            uint8_t* dst = sW + s * STAGE + i * (STAGE / nload) + crank * part * 128;
+            if constexpr (CL > 1)
+              tma_load_2d_mc(dst, m, &wfull[s], c0 + i * step_c0, c1 + crank * part, CL_MASK);
+            else
+              tma_load_2d(dst, m, &wfull[s], c0 + i * step_c0, c1);
+          }
         }
         ++ws;
       };
@@ -209,8 +235,13 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         w1(0);
         mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's epilogue left the buffer
         MTR(8, local);
-        mbar_expect_tx(xfull, X_BYTES);
-        for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmX, xfull, kb * 64, tile * BM);
+        if constexpr (PAIR) {
+          if (leader) mbar_expect_tx(xfull, 2 * X_BYTES);
+          for (int kb = 0; kb < 6; ++kb) tma_load_2d_2sm(sX + kb * X_ATOM, &tmX, lead(xfull), kb * 64, tile * BM);
+        } else {
+          mbar_expect_tx(xfull, X_BYTES);
+          for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmX, xfull, kb * 64, tile * BM);
+        }
         w1(1);
         for (int c = 0; c < NCH; ++c) {
           // L2 prefetch of what the tile boundary waits on: this tile's residual rows and
@@ -231,9 +262,9 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc1 = idesc_bf16_f32(128, HC);
-    constexpr uint32_t idesc2 = idesc_bf16_f32(128, 192);
+    // ------------------------------------------------------------ MMA issuer (the pair's leader)
+    constexpr uint32_t idesc1 = idesc_bf16_f32(PAIR ? 256 : 128, HC);
+    constexpr uint32_t idesc2 = idesc_bf16_f32(PAIR ? 256 : 128, 192);
     const uint32_t sX0 = smem_u32(sX), sW0 = smem_u32(sW), sH0 = smem_u32(sH);
     int ws = 0, g1 = 0, g2 = 0, local = 0;  // weight blocks consumed, fc1 chunks issued, fc2 chunks issued
     auto take = [&]() {
@@ -244,22 +275,43 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       tc_fence_after();
       return s;
     };
+    auto commit = [&](uint64_t* bar) {  // arrive on this barrier in every CTA of the cluster
+      if constexpr (PAIR)
+        mma_commit_2sm_mc(bar, CL_MASK);
+      else if constexpr (CL > 1)
+        mma_commit_mc(bar, CL_MASK);
+      else
+        mma_commit(bar);
+    };
+    auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, bool acc) {
+      if constexpr (PAIR)
+        mma_bf16_ss_2sm(d, ad, bd, idesc, acc);
+      else
+        mma_bf16_ss(d, ad, bd, idesc, acc);
+    };
+    // leader-owned barriers with arrivals from both CTAs: cluster-scope acquire
+    auto wait_pair = [&](uint64_t* bar, uint32_t parity) {
+      if constexpr (PAIR)
+        mbar_wait_cluster(bar, parity);
+      else
+        mbar_wait(bar, parity);
+    };
     auto give = [&](int s) {
       if (elect_one()) {
-        if constexpr (CL > 1)
-          mma_commit_mc(&wempty[s], CL_MASK);  // the slot is refilled for the whole cluster
+        if constexpr (PAIR || CL > 1)
+          commit(&wempty[s]);  // the slot is refilled in every CTA
         else
           mma_commit(&wempty[s]);
       }
       __syncwarp();
       ++ws;
     };
-    for (int tile = tile0; tile < tiles; tile += tstride, ++local) {
+    for (int tile = tile0; tile < (PAIR && !leader ? tile0 : tiles); tile += tstride, ++local) {
       mbar_wait(xfull, local & 1);
       auto fc1 = [&](int c) {
         const int b = g1 & 1;
         if (lane == 0) MTR(0, g1);
-        mbar_wait(&a1empty[b], ((g1 >> 1) & 1) ^ 1);  // GELU warps drained this buffer
+        wait_pair(&a1empty[b], ((g1 >> 1) & 1) ^ 1);  // GELU warps drained this buffer
         if (lane == 0) MTR(1, g1);
         for (int half = 0; half < 2; ++half) {
           const int s = take();
@@ -268,27 +320,27 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
             for (int a = 0; a < 3; ++a) {
               const int kb = 3 * half + a;
               const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
-              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE + a * (HC * 128));
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE + a * (HC / WSPLIT * 128));
 #pragma unroll
-              for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + ACC1 + 64 * b, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k) mma(tmem + ACC1 + 64 * b, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0);
             }
           }
           __syncwarp();
           give(s);
         }
         if (c == NCH - 1) {
-          if (elect_one()) mma_commit(xempty);  // X tile fully consumed
+          if (elect_one()) commit(xempty);  // X tile fully consumed
           __syncwarp();
         }
-        if (elect_one()) mma_commit(&a1full[b]);
+        if (elect_one()) commit(&a1full[b]);
         __syncwarp();
         ++g1;
       };
       auto fc2 = [&](int c) {
         const int b = g2 & 1;
-        if (c == 0) mbar_wait(a2empty, (local & 1) ^ 1);  // epilogue drained the previous tile
+        if (c == 0) wait_pair(a2empty, (local & 1) ^ 1);  // epilogue drained the previous tile
         if (lane == 0) MTR(2, g2);
-        mbar_wait(&hfull[b], (g2 >> 1) & 1);
+        wait_pair(&hfull[b], (g2 >> 1) & 1);
         if (lane == 0) MTR(3, g2);
         tc_fence_after();
         for (int half = 0; half < 2; ++half) {
@@ -298,14 +350,14 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
             const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16_ss(tmem + ACC2 + 192 * half, ad + 2 * k, bd + 2 * k, idesc2, (c | k) != 0);
+              mma(tmem + ACC2 + 192 * half, ad + 2 * k, bd + 2 * k, idesc2, (c | k) != 0);
           }
           __syncwarp();
           give(s);
         }
         if (elect_one()) {
-          mma_commit(&hempty[b]);
-          if (c == NCH - 1) mma_commit(a2full);
+          commit(&hempty[b]);
+          if (c == NCH - 1) commit(a2full);
         }
         __syncwarp();
         ++g2;
@@ -369,7 +421,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
             tmem_ld_wait();
             if (h + 1 == GCOLS / 32) {
               tc_fence_before();
-              mbar_arrive(&a1empty[b]);
+              if constexpr (PAIR)
+                mbar_arrive_cluster(lead(&a1empty[b]));
+              else
+                mbar_arrive(&a1empty[b]);
             }
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -388,7 +443,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
                 make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           }
           fence_proxy_async_smem();
-          mbar_arrive(&hfull[b]);
+          if constexpr (PAIR)
+            mbar_arrive_cluster(lead(&hfull[b]));  // the leader's pair MMA reads this CTA's H
+          else
+            mbar_arrive(&hfull[b]);
           if (warp == 2 && lane == 0) MTR(5, g);
         }
       }
@@ -420,7 +478,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         tmem_ld_wait();
         if (q + 1 == NQ) {
           tc_fence_before();
-          mbar_arrive(a2empty);  // accumulator drained: the next tile's fc2 may start
+          if constexpr (PAIR)
+            mbar_arrive_cluster(lead(a2empty));  // accumulator drained: the next tile's fc2 may start
+          else
+            mbar_arrive(a2empty);
         }
         const float* vb = sVec + col0 + 32 * q;
         const float* vg = sVec + D + col0 + 32 * q;
@@ -483,8 +544,13 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
   if constexpr (CL > 1) cluster_sync_all();  // peers still multicast into / arrive on this CTA until done
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_dealloc_2sm<512>(tmem);
+    else
+      tmem_dealloc<512>(tmem);
+  }
 }
 
 }  // namespace mlp
@@ -509,7 +575,7 @@ int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const 
   rc |= make_tmap_bf16_2d(&tr, xres, D, (uint64_t)M, D, 64, BM, 128);
   rc |= make_tmap_bf16_2d(&trs, xres, D, (uint64_t)M, D, 64, 32, 128);
   rc |= make_tmap_bf16_2d(&tms, xmod_out, D, (uint64_t)M, D, 64, 32, 128);
-  rc |= make_tmap_bf16_2d(&t1, w1, D, FF, D, 64, HC / CL, 128);
+  rc |= make_tmap_bf16_2d(&t1, w1, D, FF, D, 64, HC / CL, 128);  // CL = 2: each CTA loads half the rows
   rc |= make_tmap_bf16_2d(&t2, w2, FF, D, FF, 64, 192 / CL, 128);
   if (rc != SF_OK) return SF_ERR_CUDA;
   Params p{b1, b2, xres, xmod_out, gate, shift, scale, vec_stride, ln_eps, T, (int)M};
