@@ -5,7 +5,7 @@ OUT=${OUT:-gpurun_out/sweep.jsonl}
 : > $OUT
 for args in "--guidance 7.5 --n 4" "--guidance 7.5 --n 2" "--guidance 7.5 --n 1" "--n 2" "--n 1" \
             "--streams 8" "--streams 16" "--streams 64"; do
-  timeout 300 python bench.py $args --steps 20 --warmup 4 --no-cpu-baseline 2>/dev/null | tail -1 >> $OUT
+  timeout 300 python bench.py $args --steps 20 --warmup 4 --no-cpu-baseline --no-decode 2>/dev/null | tail -1 >> $OUT
 done
 python - <<'PY'
 import json
