@@ -45,13 +45,17 @@ __device__ long long g_mlp_trace[16 * 64];
 #ifndef SF_MLP_PAIR
 #define SF_MLP_PAIR 0  // 2-CTA pairs (measured slower: 384 vs 315 us; cross-CTA GELU handoffs): cta_group::2 MMAs (M=256), the weight operand split between the SMs
 #endif
-constexpr int D = 384, FF = 1536, BM = 128, HC = 64, NCH = FF / HC;  // 24 hidden chunks
+#ifndef SF_MLP_HC
+#define SF_MLP_HC 128  // hidden columns per chunk: 128 (one TMEM / smem buffer; 275 us) or 64 (two; 317 us)
+#endif
+constexpr int D = 384, FF = 1536, BM = 128, HC = SF_MLP_HC, NCH = FF / HC;
+constexpr int NB = HC == 64 ? 2 : 1;  // fc1 accumulator and H buffers
 constexpr int X_ATOM = BM * 64 * 2;                                   // 16 KB: 128 rows x 64 K
 constexpr int X_BYTES = 6 * X_ATOM;                                   // 96 KB
 constexpr int WBLOCK = 24576;                                         // 24 KB weight block (both CTAs)
-constexpr int STAGE = WBLOCK / (SF_MLP_PAIR ? 2 : 1);                  // this CTA's share
-constexpr int NSTAGE = SF_MLP_PAIR ? 6 : 3;
-constexpr int H_BYTES = BM * HC * 2;  // 16 KB
+constexpr int STAGE = HC == 128 ? 16384 : WBLOCK / (SF_MLP_PAIR ? 2 : 1);  // this CTA's share
+constexpr int NSTAGE = HC == 128 ? 4 : (SF_MLP_PAIR ? 6 : 3);
+constexpr int H_BYTES = BM * HC * 2;  // 16 / 32 KB
 #ifndef SF_MLP_GELU_WARPS
 #define SF_MLP_GELU_WARPS 8
 #endif
@@ -79,7 +83,8 @@ constexpr int ECOLS = D / PARTS;                  // output columns per epilogue
 constexpr int GCOLS = HC / (GELU_WARPS / 4);  // hidden columns per GELU thread
 constexpr int THREADS = 32 * (2 + GELU_WARPS + EPI_WARPS);
 constexpr int ACC2 = 0, ACC1 = 384;
-constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + 2 * H_BYTES + 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 256;
+constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + NB * H_BYTES + 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 256;
+static_assert(HC == 64 || (HC == 128 && !SF_MLP_PAIR && SF_MLP_CL == 1), "128-column chunks: single CTA");
 
 // 2-D TMA load multicast to the CTAs of `mask` (same smem offset and barrier in each).
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
@@ -128,7 +133,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   uint8_t* sX = smem;
   uint8_t* sW = sX + X_BYTES;
   uint8_t* sH = sW + NSTAGE * STAGE;
-  float* sVec = reinterpret_cast<float*>(sH + 2 * H_BYTES);  // b2 | gate | shift | scale  [4][384]
+  float* sVec = reinterpret_cast<float*>(sH + NB * H_BYTES);  // b2 | gate | shift | scale  [4][384]
   float* sRed = sVec + 4 * D;                                 // [2 stats][<= 4 parts][128 rows]
   float* sB1 = sRed + 2 * 4 * BM;                             // fc1 bias [1536]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB1 + FF);
@@ -222,17 +227,27 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         ++ws;
       };
       int local = 0;
-      auto w1 = [&](int c) {  // W1 rows [64c, 64c+64), K halves of 192 (3 atoms of 8 KB each)
-        wblock(&tmW1, 0, c * HC, 3, 64, HC);
-        wblock(&tmW1, 192, c * HC, 3, 64, HC);
+      auto w1 = [&](int c) {
+        if constexpr (HC == 128) {  // W1 rows [128c, +128): one 16 KB K-atom per stage
+          for (int kb = 0; kb < 6; ++kb) wblock(&tmW1, kb * 64, c * HC, 1, 0, HC);
+        } else {  // W1 rows [64c, 64c+64), K halves of 192 (3 atoms of 8 KB each)
+          wblock(&tmW1, 0, c * HC, 3, 64, HC);
+          wblock(&tmW1, 192, c * HC, 3, 64, HC);
+        }
       };
-      auto w2 = [&](int c) {  // W2 rows [0,192) and [192,384), K columns [64c, 64c+64)
-        wblock(&tmW2, c * HC, 0, 1, 0, 192);
-        wblock(&tmW2, c * HC, 192, 1, 0, 192);
+      auto w2 = [&](int c) {
+        if constexpr (HC == 128) {  // W2 rows [128n, +128) x K atom a of the chunk
+          for (int n = 0; n < 3; ++n)
+            for (int a = 0; a < 2; ++a) wblock(&tmW2, c * HC + 64 * a, 128 * n, 1, 0, 128);
+        } else {  // W2 rows [0,192) and [192,384), K columns [64c, 64c+64)
+          wblock(&tmW2, c * HC, 0, 1, 0, 192);
+          wblock(&tmW2, c * HC, 192, 1, 0, 192);
+        }
       };
       for (int tile = tile0; tile < tiles; tile += tstride, ++local) {
-        // the X buffer: X(tile) for fc1, then the tile's residual rows for the epilogue
-        w1(0);
+        // the X buffer: X(tile) for fc1, then the tile's residual rows for the epilogue.
+        // W1(0) is requested first (it fits the ring) so it lands during the previous epilogue.
+        if constexpr (HC == 64) w1(0);
         mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's epilogue left the buffer
         MTR(8, local);
         if constexpr (PAIR) {
@@ -242,6 +257,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
           mbar_expect_tx(xfull, X_BYTES);
           for (int kb = 0; kb < 6; ++kb) tma_load_2d(sX + kb * X_ATOM, &tmX, xfull, kb * 64, tile * BM);
         }
+        if constexpr (HC == 128) w1(0);  // six 16 KB blocks: more than the ring holds
         w1(1);
         for (int c = 0; c < NCH; ++c) {
           // L2 prefetch of what the tile boundary waits on: this tile's residual rows and
@@ -264,7 +280,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (the pair's leader)
     constexpr uint32_t idesc1 = idesc_bf16_f32(PAIR ? 256 : 128, HC);
-    constexpr uint32_t idesc2 = idesc_bf16_f32(PAIR ? 256 : 128, 192);
+    constexpr uint32_t idesc2 = idesc_bf16_f32(PAIR ? 256 : 128, HC == 128 ? 128 : 192);
     const uint32_t sX0 = smem_u32(sX), sW0 = smem_u32(sW), sH0 = smem_u32(sH);
     int ws = 0, g1 = 0, g2 = 0, local = 0;  // weight blocks consumed, fc1 chunks issued, fc2 chunks issued
     auto take = [&]() {
@@ -309,24 +325,38 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
     for (int tile = tile0; tile < (PAIR && !leader ? tile0 : tiles); tile += tstride, ++local) {
       mbar_wait(xfull, local & 1);
       auto fc1 = [&](int c) {
-        const int b = g1 & 1;
+        const int b = g1 % NB;
         if (lane == 0) MTR(0, g1);
-        wait_pair(&a1empty[b], ((g1 >> 1) & 1) ^ 1);  // GELU warps drained this buffer
+        wait_pair(&a1empty[b], ((g1 / NB) & 1) ^ 1);  // GELU warps drained this buffer
         if (lane == 0) MTR(1, g1);
-        for (int half = 0; half < 2; ++half) {
-          const int s = take();
-          if (elect_one()) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const int kb = 3 * half + a;
+        if constexpr (HC == 128) {
+          for (int kb = 0; kb < 6; ++kb) {
+            const int s = take();
+            if (elect_one()) {
               const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
-              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE + a * (HC / WSPLIT * 128));
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
 #pragma unroll
-              for (int k = 0; k < 4; ++k) mma(tmem + ACC1 + 64 * b, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k) mma(tmem + ACC1, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0);
             }
+            __syncwarp();
+            give(s);
           }
-          __syncwarp();
-          give(s);
+        } else {
+          for (int half = 0; half < 2; ++half) {
+            const int s = take();
+            if (elect_one()) {
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                const int kb = 3 * half + a;
+                const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
+                const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE + a * (HC / WSPLIT * 128));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma(tmem + ACC1 + 64 * b, ad + 2 * k, bd + 2 * k, idesc1, (kb | k) != 0);
+              }
+            }
+            __syncwarp();
+            give(s);
+          }
         }
         if (c == NCH - 1) {
           if (elect_one()) commit(xempty);  // X tile fully consumed
@@ -337,23 +367,38 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         ++g1;
       };
       auto fc2 = [&](int c) {
-        const int b = g2 & 1;
+        const int b = g2 % NB;
         if (c == 0) wait_pair(a2empty, (local & 1) ^ 1);  // epilogue drained the previous tile
         if (lane == 0) MTR(2, g2);
-        wait_pair(&hfull[b], (g2 >> 1) & 1);
+        wait_pair(&hfull[b], (g2 / NB) & 1);
         if (lane == 0) MTR(3, g2);
         tc_fence_after();
-        for (int half = 0; half < 2; ++half) {
-          const int s = take();
-          if (elect_one()) {
-            const uint64_t ad = sw128_kmajor_desc(sH0 + b * H_BYTES);
-            const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
+        if constexpr (HC == 128) {
+          for (int n = 0; n < 3; ++n)
+            for (int a = 0; a < 2; ++a) {
+              const int s = take();
+              if (elect_one()) {
+                const uint64_t ad = sw128_kmajor_desc(sH0 + a * X_ATOM);
+                const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma(tmem + ACC2 + 192 * half, ad + 2 * k, bd + 2 * k, idesc2, (c | k) != 0);
+                for (int k = 0; k < 4; ++k) mma(tmem + ACC2 + 128 * n, ad + 2 * k, bd + 2 * k, idesc2, (c | a | k) != 0);
+              }
+              __syncwarp();
+              give(s);
+            }
+        } else {
+          for (int half = 0; half < 2; ++half) {
+            const int s = take();
+            if (elect_one()) {
+              const uint64_t ad = sw128_kmajor_desc(sH0 + b * H_BYTES);
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma(tmem + ACC2 + 192 * half, ad + 2 * k, bd + 2 * k, idesc2, (c | k) != 0);
+            }
+            __syncwarp();
+            give(s);
           }
-          __syncwarp();
-          give(s);
         }
         if (elect_one()) {
           commit(&hempty[b]);
@@ -407,8 +452,8 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
     for (int tile = tile0; tile < tiles; tile += tstride, ++local) {
       if (is_gelu) {
         for (int c = 0; c < NCH; ++c, ++g) {
-          const int b = g & 1;
-          mbar_wait(&a1full[b], (g >> 1) & 1);
+          const int b = g % NB;
+          mbar_wait(&a1full[b], (g / NB) & 1);
           if (warp == 2 && lane == 0) MTR(4, g);
           tc_fence_after();
           // 32 columns at a time (register budget); the TMEM buffer is released after the last read
@@ -417,7 +462,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
 #pragma unroll
           for (int h = 0; h < GCOLS / 32; ++h) {
             float v[32];
-            tmem_ld32(gaddr + 64 * b + 32 * h, v);
+            tmem_ld32(gaddr + HC * b + 32 * h, v);
             tmem_ld_wait();
             if (h + 1 == GCOLS / 32) {
               tc_fence_before();
@@ -434,12 +479,14 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
               pk[16 * h + i] = pack_bf16(y.x, y.y);
             }
           }
-          mbar_wait(&hempty[b], ((g >> 1) & 1) ^ 1);  // fc2 read this buffer two chunks ago
+          mbar_wait(&hempty[b], ((g / NB) & 1) ^ 1);  // fc2 has read this buffer
+          // this thread's GCOLS columns: 16-byte chunks of its row in the 64-column H atom(s)
           uint8_t* hrow = sH + b * H_BYTES + row * 128;
 #pragma unroll
           for (int j = 0; j < GCOLS / 8; ++j) {
-            const int cj = gpart * (GCOLS / 8) + j;  // 16-byte chunk of the 128-byte row
-            *reinterpret_cast<uint4*>(hrow + ((cj ^ (row & 7)) * 16)) =
+            const int col = gpart * GCOLS + 8 * j;
+            const int at = col >> 6, cj = (col & 63) >> 3;
+            *reinterpret_cast<uint4*>(hrow + at * X_ATOM + ((cj ^ (row & 7)) * 16)) =
                 make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           }
           fence_proxy_async_smem();
@@ -576,7 +623,7 @@ int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const 
   rc |= make_tmap_bf16_2d(&trs, xres, D, (uint64_t)M, D, 64, 32, 128);
   rc |= make_tmap_bf16_2d(&tms, xmod_out, D, (uint64_t)M, D, 64, 32, 128);
   rc |= make_tmap_bf16_2d(&t1, w1, D, FF, D, 64, HC / CL, 128);  // CL = 2: each CTA loads half the rows
-  rc |= make_tmap_bf16_2d(&t2, w2, FF, D, FF, 64, 192 / CL, 128);
+  rc |= make_tmap_bf16_2d(&t2, w2, FF, D, FF, 64, (HC == 128 ? 128 : 192) / CL, 128);
   if (rc != SF_OK) return SF_ERR_CUDA;
   Params p{b1, b2, xres, xmod_out, gate, shift, scale, vec_stride, ln_eps, T, (int)M};
   static int sms = 0;
