@@ -51,10 +51,10 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
 
 int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M,
                    int32_t heads, int32_t T, int32_t hd, float q_scale, void* stream) {
-  const int bn = hd == 64 ? 192 : 144;
+  const int bn = hd == 64 ? qkv_bn64() : 144;
   const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
   if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
-  const bool two = g_gemm_2sm && hd == 64;
+  const bool two = g_gemm_2sm && hd == 64 && bn == 192;
   GemmMaps maps;
   if ((two ? make_operand_maps_2sm(&maps, A, M, K, W, N, bn) : make_operand_maps(&maps, A, M, K, W, N, bn)) != SF_OK)
     return SF_ERR_CUDA;

@@ -603,7 +603,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.q_scale = 1.0f / sqrtf((float)hd);
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_QKV, hd == 64 ? 192 : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_QKV, hd == 64 ? qkv_bn64() : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
       mark(h, P_QKV, st);
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
@@ -750,7 +750,7 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     const __nv_bfloat16* fc1 = (const __nv_bfloat16*)w->fc1_w + (int64_t)l * c.mlp_hidden * H;
     const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
     const int hd = H / c.heads;
-    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? 192 : 144);
+    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? qkv_bn64() : 144);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
     rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
     rc |= make_out_map32(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);  // 256-wide GELU tiles: 32-column chunks

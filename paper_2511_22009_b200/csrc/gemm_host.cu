@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <cstdio>
 // Host side of the tcgen05 GEMM: TMA descriptor encoding + launch dispatch.
 #include <cudaTypedefs.h>
@@ -92,13 +93,24 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
+// QKV tile width for head dim 64 (192: 4 epilogue warps, 3 heads per tile; 128: 8 warps,
+// 2 heads); SF_QKV_BN in the environment overrides for experiments.
+int qkv_bn64() {
+  static int bn = 0;
+  if (!bn) {
+    const char* e = getenv("SF_QKV_BN");
+    bn = (e && atoi(e) == 128) ? 128 : 192;
+  }
+  return bn;
+}
+
 #ifndef SF_QKV_WARPS
 #define SF_QKV_WARPS 4  // epilogue warps of the head-dim-64 QKV GEMM (4 or 12)
 #endif
 template <int BN, int KIND>
 constexpr int epi_warps() {
   // QKV: 4; RES_LN: 12; bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
-  return KIND == EPI_QKV ? (BN == 192 ? SF_QKV_WARPS : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+  return KIND == EPI_QKV ? (BN == 192 ? SF_QKV_WARPS : BN == 128 ? 8 : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
 }
 
 // Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).
@@ -150,6 +162,7 @@ int prepare_gemm_kernels() {
   rc |= set_attr<256, EPI_BF16>();
   rc |= set_attr<256, EPI_GELU>();
   rc |= set_attr<192, EPI_QKV>();
+  rc |= set_attr<128, EPI_QKV>();
   rc |= set_attr<384, EPI_RES_LN>();
   rc |= set_attr<144, EPI_QKV>();
   rc |= set_attr<128, EPI_RES>();
@@ -263,6 +276,7 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
   SF_CASE(256, EPI_BF16)
   SF_CASE(256, EPI_GELU)
   SF_CASE(192, EPI_QKV)
+  SF_CASE(128, EPI_QKV)
   SF_CASE(384, EPI_RES_LN)
   SF_CASE(144, EPI_QKV)
   SF_CASE(128, EPI_RES)

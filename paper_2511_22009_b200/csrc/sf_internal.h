@@ -41,5 +41,7 @@ int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const 
                      __nv_bfloat16* xres, __nv_bfloat16* xmod_out, const float* gate, const float* shift,
                      const float* scale, int64_t vec_stride, float ln_eps, int64_t M, int T, cudaStream_t st);
 
+int qkv_bn64();
+
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
 }  // namespace sf
