@@ -181,6 +181,14 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
 int sf_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const float* b1, const float* b2, void* xres,
                  void* xmod_out, const float* gate, const float* shift, const float* scale, int64_t vec_stride,
                  float ln_eps, int64_t M, int32_t tokens_per_slot, void* stream);
+/* Post-attention half of a DiT-S/2 block in one kernel: attention projection + gated residual
+ * + LayerNorm/modulate (kept on chip) + the fused MLP + gated residual + next LayerNorm/modulate.
+ * attn [M, 384] bf16; wproj [384, 384]; xres updated in place; xmod_out = next LN output. */
+int sf_block_tail(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
+                  const float* b1, const float* b2, void* xres, void* xmod_out, const float* gate_msa,
+                  const float* shift_mlp, const float* scale_mlp, const float* gate_mlp, const float* shift_next,
+                  const float* scale_next, int64_t vec_stride, float ln_eps, int64_t M, int32_t tokens_per_slot,
+                  void* stream);
 
 /* K6 -- flash attention, T tokens per row (multiple of 256), head dim 64, no mask.
  * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T] fp16;

@@ -42,6 +42,11 @@ int launch_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const 
                      const float* scale, int64_t vec_stride, float ln_eps, int64_t M, int T, cudaStream_t st);
 
 int qkv_bn64();
+int launch_block_tail(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
+                      const float* b1, const float* b2, __nv_bfloat16* xres, __nv_bfloat16* xmod_out,
+                      const float* gate1, const float* shift1, const float* scale1, const float* gate2,
+                      const float* shift2, const float* scale2, int64_t vec_stride, float ln_eps, int64_t M, int T,
+                      cudaStream_t st);
 
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
 }  // namespace sf

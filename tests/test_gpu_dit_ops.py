@@ -148,3 +148,49 @@ def test_mlp_fused_matches_unfused(rows):
         assert (got_m.float() - ref).abs().max().item() < 5e-2 * max(1.0, ref.abs().max().item())
     # fused and unfused agree to bf16 rounding of the same hidden
     assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, y.abs().max().item())
+
+
+@pytest.mark.parametrize("rows", [1, 2])
+def test_block_tail_matches_proj_plus_mlp(rows):
+    """sf_block_tail (projection + residual + LN + fused MLP + residual + LN in one kernel) vs
+    the two-kernel path sf_gemm_res_ln (projection) -> sf_mlp_fused, and vs torch fp32."""
+    T, N, F = 1024, 384, 1536
+    M = rows * T
+    g = torch.Generator(device="cuda").manual_seed(70 + rows)
+    attn = bf(torch.randn(M, N, device="cuda", generator=g))
+    wp = bf(torch.randn(N, N, device="cuda", generator=g) * 0.05)
+    bp = torch.randn(N, device="cuda", generator=g) * 0.1
+    w1 = bf(torch.randn(F, N, device="cuda", generator=g) * 0.05)
+    b1 = torch.randn(F, device="cuda", generator=g) * 0.1
+    w2 = bf(torch.randn(N, F, device="cuda", generator=g) * 0.03)
+    b2 = torch.randn(N, device="cuda", generator=g) * 0.1
+    xres0 = bf(torch.randn(M, N, device="cuda", generator=g))
+    vs = 8 * N
+    vecs = torch.randn(rows, vs, device="cuda", generator=g) * 0.5
+    g1, sh1, sc1 = vecs[:, 0:N], vecs[:, N:2 * N], vecs[:, 2 * N:3 * N]
+    g2, sh2, sc2 = vecs[:, 3 * N:4 * N], vecs[:, 4 * N:5 * N], vecs[:, 5 * N:6 * N]
+    ptr = lambda t: t.data_ptr()
+    # one kernel
+    xres = xres0.clone()
+    xmod = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_block_tail", ptr(attn), ptr(wp), ptr(bp), ptr(w1), ptr(w2), ptr(b1), ptr(b2), ptr(xres), ptr(xmod),
+             ptr(g1), ptr(sh1), ptr(sc1), ptr(g2), ptr(sh2), ptr(sc2), vs, 1e-6, M, T, st())
+    # two kernels
+    xres_u = xres0.clone()
+    xmod_u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    L().call("sf_gemm_res_ln", ptr(attn), ptr(wp), ptr(bp), ptr(xres_u), ptr(xmod_u), ptr(g1), ptr(sh1), ptr(sc1),
+             vs, M, N, N, T, 1e-6, st())
+    L().call("sf_mlp_fused", ptr(xmod_u), ptr(w1), ptr(w2), ptr(b1), ptr(b2), ptr(xres_u), ptr(xmod_u), ptr(g2),
+             ptr(sh2), ptr(sc2), vs, 1e-6, M, T, st())
+    torch.cuda.synchronize()
+    slot = torch.arange(M, device="cuda") // T
+    ln = lambda x: torch.nn.functional.layer_norm(x, (N,), eps=1e-6)
+    x1 = xres0.float() + g1[slot] * (attn.float() @ wp.float().t() + bp)
+    h = (ln(x1) * (1 + sc1[slot]) + sh1[slot]).to(torch.bfloat16).float()
+    hh = torch.nn.functional.gelu(h @ w1.float().t() + b1, approximate="tanh").to(torch.bfloat16).float()
+    x2 = x1 + g2[slot] * (hh @ w2.float().t() + b2)
+    out = ln(x2) * (1 + sc2[slot]) + sh2[slot]
+    for r, m in ((xres, xmod), (xres_u, xmod_u)):
+        assert (r.float() - x2).abs().max().item() < 3e-2 * max(1.0, x2.abs().max().item())
+        assert (m.float() - out).abs().max().item() < 5e-2 * max(1.0, out.abs().max().item())
+    assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, x2.abs().max().item())

@@ -52,3 +52,28 @@ fl = 2 * 2.0 * M * N * F
 for name, fn in (("fused", fused), ("unfused", unfused)):
     us = timeit(fn)
     print(f"mlp {name:8s}: {us:8.1f} us  {fl / us / 1e6:7.1f} TFLOP/s")
+
+# post-attention block tail (projection + MLP) vs the projection GEMM + fused MLP
+attn = bf(torch.randn(M, N, device="cuda"))
+wp = bf(torch.randn(N, N, device="cuda") * 0.05)
+bp = torch.zeros(N, device="cuda")
+v8 = torch.randn(M // T, 8 * N, device="cuda") * 0.1
+
+
+def tail():
+    _lib.call("sf_block_tail", attn.data_ptr(), wp.data_ptr(), bp.data_ptr(), w1.data_ptr(), w2.data_ptr(),
+              b1.data_ptr(), b2.data_ptr(), xres.data_ptr(), xmod.data_ptr(), v8.data_ptr(), v8[:, N:].data_ptr(),
+              v8[:, 2 * N:].data_ptr(), v8[:, 3 * N:].data_ptr(), v8[:, 4 * N:].data_ptr(), v8[:, 5 * N:].data_ptr(),
+              8 * N, 1e-6, M, T, st)
+
+
+def two():
+    _lib.call("sf_gemm_res_ln", attn.data_ptr(), wp.data_ptr(), bp.data_ptr(), xres.data_ptr(), xmod.data_ptr(),
+              v8.data_ptr(), v8[:, N:].data_ptr(), v8[:, 2 * N:].data_ptr(), 8 * N, M, N, N, T, 1e-6, st)
+    fused()
+
+
+fl2 = fl + 2.0 * M * N * N
+for name, fn in (("tail", tail), ("proj+mlp", two)):
+    us = timeit(fn)
+    print(f"block {name:8s}: {us:8.1f} us  {fl2 / us / 1e6:7.1f} TFLOP/s")

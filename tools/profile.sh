@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 python tools/summarize_launches.py $OUT/${TAG}_launches.csv > $OUT/${TAG}_launches.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:attn -s 2 -c 1 -o $OUT/${TAG}_attn -f $STEP > $OUT/${TAG}_attn.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm -s 1 -c 4 -o $OUT/${TAG}_gemm -f $STEP > $OUT/${TAG}_gemm.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:mlp_fused -s 1 -c 1 -o $OUT/${TAG}_mlp -f $STEP > $OUT/${TAG}_mlp.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"mlp_fused|block_tail" -s 1 -c 1 -o $OUT/${TAG}_mlp -f $STEP > $OUT/${TAG}_mlp.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'cond_kernel|patch_embed|final_layer' -c 3 -o $OUT/${TAG}_misc -f $STEP > $OUT/${TAG}_misc.log 2>&1
 ls -la $OUT
