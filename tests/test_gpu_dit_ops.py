@@ -194,3 +194,25 @@ def test_block_tail_matches_proj_plus_mlp(rows):
         assert (r.float() - x2).abs().max().item() < 3e-2 * max(1.0, x2.abs().max().item())
         assert (m.float() - out).abs().max().item() < 5e-2 * max(1.0, out.abs().max().item())
     assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, x2.abs().max().item())
+
+
+def test_fused_kernels_reject_bad_shapes():
+    """The fused MLP / block-tail entry points refuse row counts that are not whole
+    128-row tiles of whole slots (ParameterError, like the reference's shape checks)."""
+    from paper_2511_22009_b200.errors import ParameterError
+
+    N, F = 384, 1536
+    z = torch.zeros(256, N, device="cuda", dtype=torch.bfloat16)
+    w1 = torch.zeros(F, N, device="cuda", dtype=torch.bfloat16)
+    w2 = torch.zeros(N, F, device="cuda", dtype=torch.bfloat16)
+    b = torch.zeros(F, device="cuda")
+    v = torch.zeros(1, 8 * N, device="cuda")
+    with pytest.raises(ParameterError):  # M not a multiple of 128
+        L().call("sf_mlp_fused", z.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(), b.data_ptr(), z.data_ptr(),
+                 z.data_ptr(), v.data_ptr(), v.data_ptr(), v.data_ptr(), 8 * N, 1e-6, 200, 200, st())
+    with pytest.raises(ParameterError):  # tokens per slot not a multiple of 128
+        L().call("sf_block_tail", *([z.data_ptr()] * 2), b.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(),
+                 b.data_ptr(), z.data_ptr(), z.data_ptr(), *([v.data_ptr()] * 6), 8 * N, 1e-6, 256, 100, st())
+    with pytest.raises(ParameterError):  # null pointer
+        L().call("sf_block_tail", None, z.data_ptr(), b.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(),
+                 b.data_ptr(), z.data_ptr(), z.data_ptr(), *([v.data_ptr()] * 6), 8 * N, 1e-6, 256, 128, st())

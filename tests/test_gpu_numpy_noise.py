@@ -75,3 +75,17 @@ def test_stream_batch_device_noise_equals_host_noise(dtype):
     assert [(s, i) for s, i, _ in outs[0]] == [(s, i) for s, i, _ in outs[1]]
     for (_, _, a), (_, _, b) in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def test_c_abi_rejects_bad_arguments():
+    from paper_2511_22009_b200 import _lib
+
+    sd = torch.tensor([1], dtype=torch.int64, device="cuda")
+    out = torch.empty(1, 8, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for args in ((sd.data_ptr(), 0, 1, 0, out.data_ptr(), _lib.SF_F64, st),    # D < 1
+                 (sd.data_ptr(), -1, 1, 8, out.data_ptr(), _lib.SF_F64, st),   # gen < 0
+                 (sd.data_ptr(), 0, 1, 8, out.data_ptr(), 7, st),              # dtype
+                 (None, 0, 1, 8, out.data_ptr(), _lib.SF_F64, st)):            # null seeds
+        with pytest.raises(ParameterError):
+            _lib.call("sf_numpy_normal", *args)
