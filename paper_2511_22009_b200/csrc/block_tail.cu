@@ -35,7 +35,7 @@ constexpr int ECOLS = D / PARTS;      // 96 output columns per worker thread
 constexpr int GCOLS = HC / (GELU_WARPS / 4);  // 64 hidden columns per GELU thread
 constexpr int THREADS = 32 * (2 + WORKERS);
 constexpr int ACC2 = 0, ACC1 = 384;
-constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + H_BYTES + 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 256;
+constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + H_BYTES + 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 3 * D * 4 + 512;
 
 struct Params {
   const float* bp;  // b_proj [384]
@@ -52,13 +52,22 @@ struct Params {
   float ln_eps;
   int T;
   int M;
+  // next layer's QKV projection fused at the end of the tile (qkv != 0): xmod stays in smem
+  int qkv;
+  const float* bq;  // [1152]
+  float q_scale;
+  int heads;
 };
+constexpr int QN = 3 * D;        // 1152 QKV columns
+constexpr int QCH = QN / 128;    // 9 chunks of 128 columns (two heads each)
 
 __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // per-SMSP register file
     block_tail_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWp,
                       const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
                       const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmRs,
-                      const __grid_constant__ CUtensorMap tmMs, Params p) {
+                      const __grid_constant__ CUtensorMap tmMs, const __grid_constant__ CUtensorMap tmWq,
+                      const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;
@@ -67,7 +76,8 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   float* sVec = reinterpret_cast<float*>(sH + H_BYTES);  // bias | gate | shift | scale  [4][384]
   float* sRed = sVec + 4 * D;                            // [2 stats][PARTS][128 rows]
   float* sB1 = sRed + 2 * 4 * BM;                        // fc1 bias [1536]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB1 + FF);
+  float* sBq = sB1 + FF;                                 // QKV bias [1152]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBq + QN);
   uint64_t* wfull = bars;             // [NSTAGE]
   uint64_t* wempty = wfull + NSTAGE;  // [NSTAGE]
   uint64_t* afull = wempty + NSTAGE;  // attention rows landed in X
@@ -85,7 +95,11 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   uint64_t* r2full = a2empty + 1;     // x rows landed in X (final epilogue)
   uint64_t* xfree = r2full + 1;       // final epilogue done with X (next tile's attention may load)
   uint64_t* stored = xfree + 1;       // the projection epilogue's x stores have landed (r2 may load)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(stored + 1);
+  uint64_t* mready = stored + 1;      // (qkv) X holds the next layer's xmod
+  uint64_t* qfull = mready + 1;       // (qkv) [3] QKV chunk accumulator ready
+  uint64_t* qempty = qfull + 3;       // (qkv) [3] drained
+  uint64_t* qxfree = qempty + 3;      // (qkv) QKV MMAs done reading X
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(qxfree + 1);
 
   const uint32_t warp = warp_id(), lane = threadIdx.x & 31;
   const int tiles = p.M / BM;
@@ -106,9 +120,17 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
     mbar_init(a2empty, WORKERS * 32);
     mbar_init(xfree, WORKERS * 32);
     mbar_init(stored, WORKERS);  // one arrival per worker warp (its store-issuing lane)
+    mbar_init(mready, WORKERS * 32);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], WORKERS * 32);
+    }
+    mbar_init(qxfree, 1);
     fence_barrier_init();
   }
   for (int i = threadIdx.x; i < FF; i += THREADS) sB1[i] = p.b1[i];
+  if (p.qkv)
+    for (int i = threadIdx.x; i < QN; i += THREADS) sBq[i] = p.bq[i];
   if (warp == 1) tmem_alloc<512>(tmem_holder);
   tc_fence_before();
   __syncthreads();
@@ -140,7 +162,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       int local = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
         const int r0 = tile * BM;
-        mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's final epilogue left X
+        if (p.qkv)
+          mbar_wait(qxfree, (local & 1) ^ 1);  // previous tile's QKV MMAs left X
+        else
+          mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's final epilogue left X
         xload(&tmA, afull, r0);
         for (int n = 0; n < 3; ++n)
           for (int kb = 0; kb < 6; ++kb) wblock(&tmWp, kb * 64, 128 * n);
@@ -157,6 +182,9 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
             xload(&tmR, r2full, r0);
           }
         }
+        if (p.qkv)  // next layer's Wqkv: rows [128k, +128) x K atom kb
+          for (int k = 0; k < QCH; ++k)
+            for (int kb = 0; kb < 6; ++kb) wblock(&tmWq, kb * 64, 128 * k);
       }
     }
   } else if (warp == 1) {
@@ -179,9 +207,15 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       if (elect_one()) mma_commit(bar);
       __syncwarp();
     };
+    int gq = 0;  // QKV chunks issued
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       // projection: acc2[:, 128n:+128] = attn . Wproj[128n:+128]^T
       mbar_wait(a2empty, (local & 1) ^ 1);  // previous tile's final epilogue drained the accumulator
+      if (p.qkv && gq > 0)
+        for (int i = 1; i <= 3; ++i) {  // ... and its QKV epilogue drained the last three chunks
+          const int q = gq - i;
+          mbar_wait(&qempty[q % 3], (q / 3) & 1);
+        }
       mbar_wait(afull, local & 1);
       tc_fence_after();
       for (int n = 0; n < 3; ++n)
@@ -243,6 +277,30 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         if (c + 2 < NCH) fc1(c + 2);
       }
       g += NCH;
+      if (p.qkv) {
+        // next layer's QKV: 9 chunks of 128 columns through three 128-column TMEM buffers
+        mbar_wait(mready, local & 1);  // X holds xmod; the fc2 accumulator is drained
+        tc_fence_after();
+        for (int k = 0; k < QCH; ++k, ++gq) {
+          const int b = gq % 3;
+          mbar_wait(&qempty[b], ((gq / 3) & 1) ^ 1);
+          tc_fence_after();
+          for (int kb = 0; kb < 6; ++kb) {
+            const int s = take();
+            if (elect_one()) {
+              const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16_ss(tmem + ACC2 + 128 * b, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+            }
+            __syncwarp();
+            give(s);
+          }
+          if (k == QCH - 1) commit(qxfree);
+          commit(&qfull[b]);
+        }
+      }
     }
   } else {
     // ------------------------------------------------------------ worker warps 2..17
@@ -351,7 +409,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
         }
       }
     };
-    int g = 0, local = 0;
+    int g = 0, gq = 0, local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const int r0 = tile * BM;
       const int64_t slot = r0 / p.T;
@@ -405,8 +463,65 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       // ---- final epilogue: x' = x + gate_mlp * (acc + b2) -> xres; LN_next(x') -> xmod
       load_vecs(p.b2, p.g2, p.sh2, p.sc2, slot);
       res_ln(r0, a2full, local & 1, r2full, local & 1, [&] { mbar_arrive(a2empty); });
-      store_quarter(&tmMs, r0);
-      mbar_arrive(xfree);
+      if (!p.qkv) {
+        store_quarter(&tmMs, r0);
+        mbar_arrive(xfree);
+        continue;
+      }
+      // ---- next layer's QKV from the xmod rows in X: scatter head-major Q (scaled), K, V^T
+      fence_proxy_async_smem();  // xmod is read by the QKV MMAs (async proxy)
+      mbar_arrive(mready);
+      const int tok0 = r0 - (int)slot * p.T + quarter * 32;  // this warp's 32 tokens within the slot
+      uint8_t* stg = sH + e * 2048;                            // 32 rows x 64 B (SW64) staging
+      for (int k = 0; k < QCH; ++k, ++gq) {
+        const int b = gq % 3;
+        mbar_wait(&qfull[b], (gq / 3) & 1);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem + ((quarter * 32) << 16) + ACC2 + 128 * b + 32 * part, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&qempty[b]);
+        const int gc = 128 * k + 32 * part;  // QKV column of v[0]
+        const int which = gc / D, head = (gc - which * D) / 64, dim0 = gc & 63;
+        const float sc = which == 0 ? p.q_scale : 1.0f;
+        if (lane == 0) bulk_wait_read<0>();  // the previous chunk's store has read the staging
+        __syncwarp();
+        if (which < 2) {  // Q / K rows: 32 tokens x 32 dims (64 B, SW64)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              pk[i] = pack_bf16((v[8 * c + 2 * i] + sBq[gc + 8 * c + 2 * i]) * sc,
+                                (v[8 * c + 2 * i + 1] + sBq[gc + 8 * c + 2 * i + 1]) * sc);
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) * 16)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        } else {  // V^T rows: 32 dims x 32 tokens (fp16, 64 B, SW64)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t dd = i;
+            *reinterpret_cast<__half*>(stg + dd * 64 + (((lane >> 3) ^ ((dd >> 1) & 3)) * 16) + (lane & 7) * 2) =
+                __float2half_rn(v[i] + sBq[gc + i]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int64_t bh = slot * p.heads + head;
+          if (which == 0)
+            tma_store_2d(&tmQ, stg, dim0, (int)(bh * p.T + tok0));
+          else if (which == 1)
+            tma_store_2d(&tmK, stg, dim0, (int)(bh * p.T + tok0));
+          else
+            tma_store_2d(&tmV, stg, tok0, (int)(bh * 64 + dim0));
+          bulk_commit();
+        }
+        __syncwarp();
+      }
+      if (lane == 0) bulk_wait_read<0>();  // H is the next tile's hidden buffer
+      __syncwarp();
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
@@ -422,7 +537,8 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
                       const float* b1, const float* b2, __nv_bfloat16* xres, __nv_bfloat16* xmod_out,
                       const float* gate1, const float* shift1, const float* scale1, const float* gate2,
                       const float* shift2, const float* scale2, int64_t vec_stride, float ln_eps, int64_t M, int T,
-                      cudaStream_t st) {
+                      cudaStream_t st, const void* wqkv, const float* bqkv, void* q, void* k, void* vt, int heads,
+                      float q_scale) {
   using namespace tail;
   if (M % BM || T % BM) return SF_ERR_PARAMETER;
   static bool attr = false;
@@ -442,8 +558,19 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
   rc |= make_tmap_bf16_2d(&tr, xres, D, (uint64_t)M, D, 64, BM, 128);
   rc |= make_tmap_bf16_2d(&trs, xres, D, (uint64_t)M, D, 64, 32, 128);
   rc |= make_tmap_bf16_2d(&tms, xmod_out, D, (uint64_t)M, D, 64, 32, 128);
+  CUtensorMap twq = tp, tq = tms, tk = tms, tv = tms;  // placeholders when the QKV phase is off
+  const bool qkv = wqkv != nullptr;
+  if (qkv) {
+    if (heads * 64 != D) return SF_ERR_PARAMETER;
+    const uint64_t bh = (uint64_t)(M / T) * heads;
+    rc |= make_tmap_bf16_2d(&twq, wqkv, D, QN, D, 64, 128, 128);
+    rc |= make_tmap_bf16_2d(&tq, q, 64, bh * T, 64, 32, 32, 64);
+    rc |= make_tmap_bf16_2d(&tk, k, 64, bh * T, 64, 32, 32, 64);
+    rc |= make_tmap_bf16_2d(&tv, vt, T, bh * 64, T, 32, 32, 64);
+  }
   if (rc != SF_OK) return SF_ERR_CUDA;
-  Params p{bproj, b1, b2, xres, gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, T, (int)M};
+  Params p{bproj, b1, b2, xres, gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, T, (int)M,
+           qkv ? 1 : 0, bqkv, q_scale, heads};
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -451,7 +578,8 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = (int)(M / BM);
-  block_tail_kernel<<<tiles < sms ? tiles : sms, THREADS, SMEM, st>>>(ta, tp, t1, t2, tr, trs, tms, p);
+  block_tail_kernel<<<tiles < sms ? tiles : sms, THREADS, SMEM, st>>>(ta, tp, t1, t2, tr, trs, tms, twq, tq, tk, tv,
+                                                                      p);
   return cuda_status();
 }
 
@@ -467,5 +595,19 @@ extern "C" int sf_block_tail(const void* attn, const void* wproj, const float* b
     return SF_ERR_PARAMETER;
   return sf::launch_block_tail(attn, wproj, bproj, w1, w2, b1, b2, (__nv_bfloat16*)xres, (__nv_bfloat16*)xmod_out,
                                gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, M, T,
-                               (cudaStream_t)stream);
+                               (cudaStream_t)stream, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.f);
+}
+
+extern "C" int sf_block_tail_qkv(const void* attn, const void* wproj, const float* bproj, const void* w1,
+                                 const void* w2, const float* b1, const float* b2, void* xres, const float* gate1,
+                                 const float* shift1, const float* scale1, const float* gate2, const float* shift2,
+                                 const float* scale2, int64_t vec_stride, float ln_eps, int64_t M, int32_t T,
+                                 const void* wqkv, const float* bqkv, void* q, void* k, void* vt, int32_t heads,
+                                 float q_scale, void* stream) {
+  if (!attn || !wproj || !bproj || !w1 || !w2 || !b1 || !b2 || !xres || !gate1 || !shift1 || !scale1 || !gate2 ||
+      !shift2 || !scale2 || !wqkv || !bqkv || !q || !k || !vt || M < 1 || T < 1)
+    return SF_ERR_PARAMETER;
+  return sf::launch_block_tail(attn, wproj, bproj, w1, w2, b1, b2, (__nv_bfloat16*)xres, (__nv_bfloat16*)xres,
+                               gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, M, T,
+                               (cudaStream_t)stream, wqkv, bqkv, q, k, vt, heads, q_scale);
 }

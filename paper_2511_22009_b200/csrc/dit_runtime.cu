@@ -563,6 +563,17 @@ static bool block_tail_ok(const sf_dit_config& c) {
   return g_block_tail && mlp_fused_ok(c);
 }
 
+// The next layer's QKV projection at the end of the block tail (SF_TAIL_QKV=1; correct but
+// measured slower: 2833 vs 3019 frames/s -- the QKV phase serialises behind the tile's X buffer).
+static int g_tail_qkv = -1;
+static bool tail_qkv_ok() {
+  if (g_tail_qkv < 0) {
+    const char* e = getenv("SF_TAIL_QKV");
+    g_tail_qkv = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_tail_qkv;
+}
+
 enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_MLP, P_TAIL,
                  P_NCLS };
 
@@ -607,8 +618,9 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
   // (DiT-XL, 1152): gated-residual epilogue (RES) + a LayerNorm/modulate pass.
   const bool fused_ln = H == 384;
   int rc;
+  const bool tail_qkv = block_tail_ok(c) && tail_qkv_ok();
   for (int l = 0; l < c.depth; ++l) {
-    {
+    if (!(tail_qkv && l > 0)) {  // with tail_qkv, layer l's QKV ran in layer l-1's block tail
       EpiParams ep{};
       ep.bias = h->w.qkv_b + (int64_t)l * 3 * H;
       ep.heads = c.heads;
@@ -630,7 +642,12 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
                                   (const __nv_bfloat16*)h->w.fc2_w + (int64_t)l * H * c.mlp_hidden,
                                   h->w.fc1_b + (int64_t)l * c.mlp_hidden, h->w.fc2_b + (int64_t)l * H, h->xres,
                                   h->xmod, mb + 2 * H, mb + 3 * H, mb + 4 * H, mb + 5 * H, nxt, nxt + H,
-                                  h->mod_stride, c.ln_eps, M, T, st)))
+                                  h->mod_stride, c.ln_eps, M, T, st,
+                                  tail_qkv && l + 1 < c.depth
+                                      ? (const __nv_bfloat16*)h->w.qkv_w + (int64_t)(l + 1) * 3 * H * H
+                                      : nullptr,
+                                  h->w.qkv_b + (int64_t)(l + 1 < c.depth ? l + 1 : l) * 3 * H, h->q, h->k, h->vt,
+                                  c.heads, 1.0f / sqrtf((float)hd))))
         return rc;
       mark(h, P_TAIL, st);
       continue;
