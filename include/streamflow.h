@@ -189,6 +189,13 @@ int sf_block_tail(const void* attn, const void* wproj, const float* bproj, const
                   const float* shift_mlp, const float* scale_mlp, const float* gate_mlp, const float* shift_next,
                   const float* scale_next, int64_t vec_stride, float ln_eps, int64_t M, int32_t tokens_per_slot,
                   void* stream);
+/* Experimental (slower): sf_block_tail that also computes the next layer's QKV
+ * projection from the LayerNorm output it keeps in smem (q, k bf16 head-major, vt fp16). */
+int sf_block_tail_qkv(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
+                      const float* b1, const float* b2, void* xres, const float* gate_msa, const float* shift_mlp,
+                      const float* scale_mlp, const float* gate_mlp, const float* shift_next, const float* scale_next,
+                      int64_t vec_stride, float ln_eps, int64_t M, int32_t tokens_per_slot, const void* wqkv,
+                      const float* bqkv, void* q, void* k, void* vt, int32_t heads, float q_scale, void* stream);
 
 /* K6 -- flash attention, T tokens per row (multiple of 256), head dim 64, no mask.
  * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T] fp16;
