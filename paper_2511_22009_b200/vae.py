@@ -122,7 +122,8 @@ class TinyDecoder:
     max_frames  workspace capacity (the padded activations of all four stages, zeroed once)
     """
 
-    def __init__(self, state_dict: dict | None = None, seed: int = 0, max_frames: int = 32, device: str = "cuda"):
+    def __init__(self, state_dict: dict | None = None, seed: int = 0, max_frames: int = 32, device: str = "cuda",
+                 use_graph: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("TinyDecoder needs a CUDA device; there is no CPU fallback")
         if max_frames < 1:
@@ -149,6 +150,9 @@ class TinyDecoder:
         self._w.final_w, self._w.final_b = self.final_w.data_ptr(), self.final_b.data_ptr()
         nbytes = int(_lib.fn("sf_taesd_workspace_bytes")(self.max_frames))
         self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        # the 35-launch decode replays as one CUDA graph per (latent, image, F) binding
+        self.use_graph = bool(use_graph)
+        self._graphs: dict = {}
 
     @staticmethod
     def state_keys() -> list[str]:
@@ -177,9 +181,24 @@ class TinyDecoder:
         lat = latents.to(device=self.device, dtype=torch.float32).contiguous()
         if out is None:
             out = torch.empty(F, *IMAGE_SHAPE, dtype=torch.float32, device=self.device)
+        key = (lat.data_ptr(), out.data_ptr(), F)
+        g = self._graphs.get(key) if self.use_graph and lat is latents else None
+        if g is not None:
+            g.replay()
+            return out
+        self._launch(lat, out, F)
+        if self.use_graph and lat is latents and len(self._graphs) < 8 and not torch.cuda.is_current_stream_capturing():
+            # capture after one eager run (kernel attributes set); later calls with the same
+            # buffers replay it
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._launch(lat, out, F)
+            self._graphs[key] = g
+        return out
+
+    def _launch(self, lat: torch.Tensor, out: torch.Tensor, F: int) -> None:
         _lib.call("sf_taesd_decode", C.byref(self._w), lat.data_ptr(), F, self.max_frames,
                   self.workspace.data_ptr(), self.workspace.numel(), out.data_ptr(),
                   torch.cuda.current_stream().cuda_stream)
-        return out
 
     __call__ = decode
