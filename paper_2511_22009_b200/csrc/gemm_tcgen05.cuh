@@ -38,6 +38,9 @@ __device__ long long g_gemm_trace[8 * 64];
   } while (0)
 #endif
 
+#ifndef SF_QKV_DIAG_NOVT
+#define SF_QKV_DIAG_NOVT 0
+#endif
 enum EpiKind : int {
   EPI_F32 = 0,     // out f32 [M, ldo]  = acc + bias
   EPI_BF16 = 1,    // out bf16 [M, ldo] = acc + bias
@@ -533,8 +536,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
               *reinterpret_cast<__half*>(buf + i * 64 + ((((lane >> 3) ^ ((i >> 1) & 3))) * 16) + (lane & 7) * 2) =
                   __float2half_rn(v[i]);
           }
-          if (which < 2)
-            out.release(lane, &maps.d[which], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          if (which < 2 || SF_QKV_DIAG_NOVT)
+            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
           else
             out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 72), do_store && r0 < ep.M);
         }
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
               v[4 * i + 2] = (v[4 * i + 2] + b.z) * sc;
               v[4 * i + 3] = (v[4 * i + 3] + b.w) * sc;
             }
-            if (which < 2) {
+            if (which < 2 || SF_QKV_DIAG_NOVT) {  // (diagnostic: V stored like K, timing only)
 #pragma unroll
               for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, 4 * h + i, pack8_bf16(v + 8 * i));
             } else {
@@ -627,8 +630,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           if (c0 + 64 >= COLS) {
             acc_release(acc);
           }
-          if (which < 2)
-            out.release(lane, &maps.d[which], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          if (which < 2 || SF_QKV_DIAG_NOVT)
+            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
           else
             out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
         }
