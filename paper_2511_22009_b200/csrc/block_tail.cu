@@ -99,7 +99,9 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   uint64_t* qfull = mready + 1;       // (qkv) [3] QKV chunk accumulator ready
   uint64_t* qempty = qfull + 3;       // (qkv) [3] drained
   uint64_t* qxfree = qempty + 3;      // (qkv) QKV MMAs done reading X
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(qxfree + 1);
+  uint64_t* hafull = qxfree + 1;      // (!qkv) [2] attention K-atom landed in an H slot
+  uint64_t* haempty = hafull + 2;     // (!qkv) [2] projection MMAs done with it
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(haempty + 2);
 
   const uint32_t warp = warp_id(), lane = threadIdx.x & 31;
   const int tiles = p.M / BM;
@@ -126,6 +128,10 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       mbar_init(&qempty[i], WORKERS * 32);
     }
     mbar_init(qxfree, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hafull[i], 1);
+      mbar_init(&haempty[i], 1);
+    }
     fence_barrier_init();
   }
   for (int i = threadIdx.x; i < FF; i += THREADS) sB1[i] = p.b1[i];
@@ -162,15 +168,29 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
       int local = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
         const int r0 = tile * BM;
-        if (p.qkv)
-          mbar_wait(qxfree, (local & 1) ^ 1);  // previous tile's QKV MMAs left X
-        else
+        if (!p.qkv) {
+          // projection operands without the X buffer: attention K-atoms through the two H
+          // slots (idle between the previous tile's last fc2 and this tile's first GELU),
+          // Wproj blocks through the ring -- so this projection overlaps the previous
+          // tile's final epilogue, which still owns X
+          if (local > 0) mbar_wait(hempty, (NCH * local - 1) & 1);  // previous tile's last fc2 read H
+          for (int kb = 0; kb < 6; ++kb) {
+            const int u = local * 6 + kb, slot = kb & 1;
+            mbar_wait(&haempty[slot], ((u >> 1) & 1) ^ 1);
+            mbar_expect_tx(&hafull[slot], X_ATOM);
+            tma_load_2d(sH + slot * X_ATOM, &tmA, &hafull[slot], kb * 64, r0);
+            for (int n = 0; n < 3; ++n) wblock(&tmWp, kb * 64, 128 * n);
+          }
           mbar_wait(xfree, (local & 1) ^ 1);  // previous tile's final epilogue left X
-        xload(&tmA, afull, r0);
-        for (int n = 0; n < 3; ++n)
-          for (int kb = 0; kb < 6; ++kb) wblock(&tmWp, kb * 64, 128 * n);
-        mbar_wait(aempty, local & 1);  // projection MMAs have read the attention rows
-        xload(&tmR, r1full, r0);
+          xload(&tmR, r1full, r0);
+        } else {
+          mbar_wait(qxfree, (local & 1) ^ 1);  // previous tile's QKV MMAs left X
+          xload(&tmA, afull, r0);
+          for (int n = 0; n < 3; ++n)
+            for (int kb = 0; kb < 6; ++kb) wblock(&tmWp, kb * 64, 128 * n);
+          mbar_wait(aempty, local & 1);  // projection MMAs have read the attention rows
+          xload(&tmR, r1full, r0);
+        }
         w1(0);
         w1(1);
         for (int c = 0; c < NCH; ++c) {
@@ -216,21 +236,43 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
           const int q = gq - i;
           mbar_wait(&qempty[q % 3], (q / 3) & 1);
         }
-      mbar_wait(afull, local & 1);
-      tc_fence_after();
-      for (int n = 0; n < 3; ++n)
-        for (int kb = 0; kb < 6; ++kb) {
-          const int s = take();
-          if (elect_one()) {
-            const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
-            const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
+      if (!p.qkv) {
+        for (int kb = 0; kb < 6; ++kb) {  // A = attention K-atom kb in H slot kb & 1
+          const int u = local * 6 + kb, slot = kb & 1;
+          mbar_wait(&hafull[slot], (u >> 1) & 1);
+          tc_fence_after();
+          for (int n = 0; n < 3; ++n) {
+            const int s = take();
+            if (elect_one()) {
+              const uint64_t ad = sw128_kmajor_desc(sH0 + slot * X_ATOM);
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mma_bf16_ss(tmem + ACC2 + 128 * n, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(tmem + ACC2 + 128 * n, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            }
+            __syncwarp();
+            give(s);
           }
-          __syncwarp();
-          give(s);
+          commit(&haempty[slot]);
         }
-      commit(aempty);
+      } else {
+        mbar_wait(afull, local & 1);
+        tc_fence_after();
+        for (int n = 0; n < 3; ++n)
+          for (int kb = 0; kb < 6; ++kb) {
+            const int s = take();
+            if (elect_one()) {
+              const uint64_t ad = sw128_kmajor_desc(sX0 + kb * X_ATOM);
+              const uint64_t bd = sw128_kmajor_desc(sW0 + s * STAGE);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(tmem + ACC2 + 128 * n, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            }
+            __syncwarp();
+            give(s);
+          }
+        commit(aempty);
+      }
       commit(pfull);
       mbar_wait(xready, local & 1);  // X holds h, the projection accumulator is drained
       tc_fence_after();
