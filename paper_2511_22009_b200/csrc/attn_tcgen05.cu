@@ -36,6 +36,9 @@
 #define SF_ATTN_NOEXP 0  // diagnostics: 1 = skip exp2 (timing only, wrong results), 2 = all MUFU,
                          // 3 = softmax skipped (MMA/sync skeleton), 4 = no MMAs
 #endif
+#ifndef SF_ATTN_WARP_ARRIVE
+#define SF_ATTN_WARP_ARRIVE 0  // 1: one P-ready arrival per warp (measured 259/305 vs 252/309 us: no gain)
+#endif
 #ifndef SF_ATTN_DEFER
 #define SF_ATTN_DEFER 0  // 1: signal P(j-1) after S(j) is loaded and reduced (measured slower: 256 vs 253 us)
 #endif
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], SF_ATTN_WARP_ARRIVE ? 4 : 128);
       mbar_init(&o_full[i], 1);
     }
     for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], 128);
@@ -359,7 +362,8 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         if (lane == 0 && quarter == 0) ATR(2 * t, G);
         tc_fence_after();
 #if SF_ATTN_NOEXP == 3  // diagnostics: softmax does no work (MMA/sync skeleton alone)
-        mbar_arrive(&p_full[2 * t + b]);
+        __syncwarp();
+        if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + b]);
         continue;
 #endif
         float s[BKV];
@@ -380,7 +384,8 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         if (j > 0) {  // P_t(j-1) (stored last iteration, its latency hidden behind this S load + max)
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&p_full[2 * t + (b ^ 1)]);
+          __syncwarp();
+          if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + (b ^ 1)]);
         }
 #endif
         if (j == 0) {
@@ -436,14 +441,20 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         tmem_st_wait();
         if (lane == 0 && quarter == 0) ATR(11 + 4 * t, G);  // stores complete
         tc_fence_before();
+#if SF_ATTN_WARP_ARRIVE
+        __syncwarp();  // the warp's P stores are complete: one arrival per warp
+        if (lane == 0) mbar_arrive(&p_full[2 * t + b]);
+#else
         mbar_arrive(&p_full[2 * t + b]);
+#endif
         if (lane == 0 && quarter == 0) ATR(2 * t + 1, G);
 #endif
       }
 #if SF_ATTN_DEFER
       tmem_st_wait();  // the item's last P
       tc_fence_before();
-      mbar_arrive(&p_full[2 * t + ((nkv - 1) & 1)]);
+      __syncwarp();
+      if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + ((nkv - 1) & 1)]);
 #endif
       // epilogue: O / l -> bf16 -> out[row*T + q, head*HD ...]
       mbar_wait(&o_full[2 * t + 1], ((G - 1) >> 1) & 1);  // last PV (odd buffer); earlier PVs completed before it
