@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  grid_dep_sync();
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 8) {
@@ -529,15 +530,16 @@ int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, 
   if (prepare_attn_kernel() != SF_OK) return SF_ERR_CUDA;
   const int64_t items = rows * heads * (T / (2 * attn::BQ));
   const int grid = (int)(items < attn_sm_count() ? items : attn_sm_count());
+  cudaError_t err;
   if (m.hd == 64)
-    attn_fwd_tcgen05<64><<<grid, attn::THREADS, AttnCfg<64>::SMEM, st>>>(m.q, m.qh, m.k, m.kh, m.v, out, T, heads,
-                                                                          (int)items);
+    err = launch_maybe_pdl(attn_fwd_tcgen05<64>, dim3(grid), dim3(attn::THREADS), AttnCfg<64>::SMEM, st, m.q, m.qh,
+                           m.k, m.kh, m.v, out, T, heads, (int)items);
   else if (m.hd == 72)
-    attn_fwd_tcgen05<72><<<grid, attn::THREADS, AttnCfg<72>::SMEM, st>>>(m.q, m.qh, m.k, m.kh, m.v, out, T, heads,
-                                                                          (int)items);
+    err = launch_maybe_pdl(attn_fwd_tcgen05<72>, dim3(grid), dim3(attn::THREADS), AttnCfg<72>::SMEM, st, m.q, m.qh,
+                           m.k, m.kh, m.v, out, T, heads, (int)items);
   else
     return SF_ERR_PARAMETER;
-  return cuda_status();
+  return err == cudaSuccess ? cuda_status() : SF_ERR_CUDA;
 }
 
 }  // namespace sf

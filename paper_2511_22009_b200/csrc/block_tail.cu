@@ -146,6 +146,7 @@ __global__ void __maxnreg__(16384 / ((THREADS / 32 + 3) / 4) / 32 / 8 * 8)  // p
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  grid_dep_sync();
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
@@ -704,9 +705,9 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = (int)(M / BM);
-  block_tail_kernel<<<tiles < sms ? tiles : sms, THREADS, SMEM, st>>>(ta, tp, t1, t2, tr, trs, tms, twq, tq, tk, tv,
-                                                                      p);
-  return cuda_status();
+  const cudaError_t err = launch_maybe_pdl(block_tail_kernel, dim3(tiles < sms ? tiles : sms), dim3(THREADS), SMEM, st,
+                                           ta, tp, t1, t2, tr, trs, tms, twq, tq, tk, tv, p);
+  return err == cudaSuccess ? cuda_status() : SF_ERR_CUDA;
 }
 
 }  // namespace sf

@@ -173,6 +173,15 @@ int prepare_gemm_kernels() {
   return rc;
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SF_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on;
+}
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -213,8 +222,9 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
     err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W>, maps, N, K, e);
     if (err == cudaSuccess) err = cudaGetLastError();
   } else {
-    gemm_bf16_tcgen05<BN, KIND, W><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(maps, N, K, e);
-    err = cudaGetLastError();
+    err = launch_maybe_pdl(gemm_bf16_tcgen05<BN, KIND, W>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, maps, N,
+                           K, e);
+    if (err == cudaSuccess) err = cudaGetLastError();
   }
   if (err != cudaSuccess) {
     fprintf(stderr, "streamflow: gemm<%d,%d> launch failed: %s (smem %d, threads %d)\n", BN, KIND,

@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  grid_dep_sync();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {

@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "../../include/streamflow.h"
 
 namespace sf {
@@ -50,4 +52,28 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
                       void* k = nullptr, void* vt = nullptr, int heads = 0, float q_scale = 0.f);
 
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
+
+// Programmatic dependent launch (PDL) for the per-layer chain QKV GEMM -> attention ->
+// block tail: the next kernel's CTAs launch as the previous kernel's CTAs retire and run
+// their prologue (barrier init, TMEM alloc, descriptor prefetch) under its tail; each
+// PDL kernel executes griddepcontrol.wait before touching activations, so every kernel
+// completes only after its predecessor did (transitive ordering). SF_PDL=1 enables: measured
+// neutral (3067 vs 3080 frames/s power-capped; 2783 vs 2794 / 11180 vs 11186 at full clock on
+// the 8-stream / 1-slot configs) -- graph replay already leaves no launch gap worth hiding.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 }  // namespace sf
