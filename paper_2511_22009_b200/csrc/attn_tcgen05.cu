@@ -48,6 +48,13 @@
 #ifndef SF_ATTN_TRACE
 #define SF_ATTN_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_attn_trace_read)
 #endif
+#ifndef SF_ATTN_SATCLAMP
+#define SF_ATTN_SATCLAMP 0  // 1: polynomial exp2 input clamped by a saturating FFMA (u = sat(x/256 + 127/256));
+                            // one issue slot less per pair but measured neutral (276.3 vs 276.4 us avg, E=5/6)
+#endif
+#ifndef SF_ATTN_MAX3
+#define SF_ATTN_MAX3 1  // row max as four 3-input max chains (32+2 FMNMX3) instead of 8 + 24 + 7 (276.4 vs 279.9 us)
+#endif
 #ifndef SF_ATTN_EMU_PAIRS
 #define SF_ATTN_EMU_PAIRS 6  // exp2 pairs per 32-key chunk evaluated by polynomial (of 16)
 #endif
@@ -133,6 +140,31 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
   const float2 jf = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
   const float2 f = __ffma2_rn(jf, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(f, make_float2(0.055088773f, 0.055088773f), make_float2(0.24260406f, 0.24260406f));
+  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
+  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  const uint32_t b0 = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t b1 = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(b0), __uint_as_float(b1));
+}
+
+// Same, from raw scores s with the clamp folded into a saturating FFMA per element:
+// u = sat(s * L2E/256 + (127 - m)/256) is x = s*L2E - m clamped to [-127, 129] in units
+// of 1/256 (x <= 8 after the lazy-rescale check), x = 256u - 127 exactly enough
+// (abs. error 256 * 2^-25 in x, 1e-5 relative in 2^x); then
+//   t = 256u + (magic - 127) = magic + rint(x),  k' = (magic - 127) - t = -(rint(x) + 127),
+//   f = 256u + k' = x - rint(x):  11 issue slots per pair instead of 12.
+__device__ __forceinline__ float sat_fma(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float2 exp2_poly2_sat(float2 s, float a, float c) {
+  const float kMagic = 12582912.0f;
+  const float2 u = make_float2(sat_fma(s.x, a, c), sat_fma(s.y, a, c));
+  const float2 t = __ffma2_rn(u, make_float2(256.f, 256.f), make_float2(kMagic - 127.f, kMagic - 127.f));
+  const float2 kn = __ffma2_rn(t, make_float2(-1.f, -1.f), make_float2(kMagic - 127.f, kMagic - 127.f));
+  const float2 f = __ffma2_rn(u, make_float2(256.f, 256.f), kn);
   float2 p = __ffma2_rn(f, make_float2(0.055088773f, 0.055088773f), make_float2(0.24260406f, 0.24260406f));
   p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
   p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
@@ -372,6 +404,19 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         tmem_ld32(lane_base + S_COL(t, b) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
         tmem_ld_wait();
         if (lane == 0 && quarter == 0) ATR(8 + 4 * t, G);  // S in registers
+#if SF_ATTN_MAX3
+        // four chains of 3-input maxima over 16 scores each (7 + 1 FMNMX3 per chain), then 4 -> 1
+        float mx[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(fmaxf(s[q], s[q + 4]), s[q + 8]);
+#pragma unroll
+        for (int i = 12; i < BKV - 4; i += 8)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mx[q] = fmaxf(fmaxf(mx[q], s[i + q]), s[i + 4 + q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], s[BKV - 4 + q]);
+        const float m_tile = L2E * fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+#else
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = fmaxf(s[i], s[i + 8]);
@@ -381,6 +426,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
           for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], fmaxf(s[i + q], s[i + 8 + q]));
         const float m_tile = L2E * fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                          fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+#endif
 #if SF_ATTN_DEFER
         if (j > 0) {  // P_t(j-1) (stored last iteration, its latency hidden behind this S load + max)
           tmem_st_wait();
@@ -413,6 +459,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         }
         if (lane == 0 && quarter == 0) ATR(9 + 4 * t, G);  // max + rescale check done
         const float2 l2e2 = make_float2(L2E, L2E), negm = make_float2(-m_ref, -m_ref);
+        const float sat_c = (127.f - m_ref) * (1.f / 256.f);
 #pragma unroll
         for (int c = 0; c < BKV / 32; ++c) {
           uint32_t pk[16];
@@ -427,7 +474,11 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
             p.y = ex2(x.y);
 #else
             if (i < SF_ATTN_EMU_PAIRS) {
+#if SF_ATTN_SATCLAMP
+              p = exp2_poly2_sat(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), L2E * (1.f / 256.f), sat_c);
+#else
               p = exp2_poly2(x);
+#endif
             } else {
               p.x = ex2(x.x);
               p.y = ex2(x.y);
