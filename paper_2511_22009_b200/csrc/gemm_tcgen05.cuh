@@ -41,6 +41,15 @@ __device__ long long g_gemm_trace[8 * 64];
 #ifndef SF_QKV_DIAG_NOVT
 #define SF_QKV_DIAG_NOVT 0
 #endif
+#ifndef SF_QKV_BIAS_ALL
+#define SF_QKV_BIAS_ALL 1  // QKV epilogue: whole bias staged in smem once per CTA
+#endif
+#ifndef SF_QKV_NBUF
+#define SF_QKV_NBUF 3  // QKV epilogue: TMA-store staging buffers per warp (3: 118.7 vs 122.1 us, 4: 128.5 -- one A/B stage fewer)
+#endif
+#ifndef SF_QKV_LD64
+#define SF_QKV_LD64 1  // QKV epilogue: one TMEM-load wait per 64-column head chunk
+#endif
 enum EpiKind : int {
   EPI_F32 = 0,     // out f32 [M, ldo]  = acc + bias
   EPI_BF16 = 1,    // out bf16 [M, ldo] = acc + bias
@@ -109,7 +118,8 @@ struct GemmCfg {
   static constexpr bool LN_RING = KIND == EPI_RES_LN || KIND == EPI_RES_LN2;  // 32-column SW64 chunks
   static constexpr bool NARROW = LN_RING || ((KIND == EPI_BF16 || KIND == EPI_GELU) && EPI_WARPS == 16);
   static constexpr int OUT_BUF = BN == 144 ? 5120 : NARROW ? 2048 : 4096;
-  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : 2;  // RES_LN(2): one buffer per chunk
+  // RES_LN(2): one buffer per chunk; QKV (head dim 64): SF_QKV_NBUF store buffers per warp
+  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : (KIND == EPI_QKV && BN == 192) ? SF_QKV_NBUF : 2;
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
   static constexpr int RBAR_BYTES = EPI_WARPS * 4 * 8;  // residual-chunk barriers (one per staging buffer)
   // RES_LN2 exchange: [tile parity][pass][source CTA][column group][128 rows] floats
@@ -160,14 +170,14 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t smem_addr) {
 // Per-warp output staging: a 32-row tile in the TMA swizzle layout, 128-byte
 // rows (SW128: 16-byte chunk c of row r at c ^ (r & 7)) or 64-byte rows (SW64:
 // chunk c at c ^ ((r >> 1) & 3)).  Lane = row.
-template <int BUF>
+template <int BUF, int NB = 2>
 struct OutStageT {
-  uint8_t* base;     // this warp's 2 x BUF bytes
-  uint32_t count;    // chunks issued so far by this warp (buffer = count & 1)
+  uint8_t* base;     // this warp's NB x BUF bytes
+  uint32_t count;    // chunks issued so far by this warp (buffer = count % NB)
   __device__ __forceinline__ uint8_t* acquire(uint32_t lane) {
-    if (count >= 2 && lane == 0) bulk_wait_read<1>();  // the store issued 2 chunks ago left this buffer
+    if (count >= NB && lane == 0) bulk_wait_read<NB - 1>();  // the store issued NB chunks ago left this buffer
     __syncwarp();
-    return base + (count & 1) * BUF;
+    return base + (count % NB) * BUF;
   }
   __device__ __forceinline__ static void put16(uint8_t* buf, uint32_t row, uint32_t chunk, uint4 v) {
     if constexpr (BUF == 4096)
@@ -358,11 +368,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     constexpr int COLS = BN / (EPI_WARPS / 4);  // columns per thread (warps sharing a lane quarter split them)
     const int c_lo = (int)(e / 4) * COLS;
     const int et = threadIdx.x - 64;
-    using OutStage = OutStageT<C::OUT_BUF>;
+    using OutStage = OutStageT<C::OUT_BUF, C::LN_RING ? 2 : C::OUT_NBUF>;
     OutStage out{sOut + e * C::OUT_NBUF * C::OUT_BUF, 0};
     uint32_t ring = 0;  // RES: per-buffer load parity bits
     const bool do_store = !ep.no_store;
     uint32_t local = 0;
+    // QKV: the whole bias row (3*hidden floats) fits the vector area, so it is staged
+    // once instead of per tile (the per-tile global-load latency sat on the epilogue's
+    // critical path, which bounds this GEMM: ~4400 vs ~2900 MMA cycles per tile)
+    const bool bias_all = KIND == EPI_QKV && SF_QKV_BIAS_ALL && N * 4 <= C::VEC_BYTES;
+    if (bias_all) {
+      for (int c = et; c < N; c += EPI_THREADS) vecs[c] = ep.bias[c];
+      named_bar_sync(5, EPI_THREADS);
+    }
     for (int tile = t_first; tile < t_limit; tile += t_stride, ++local) {
       const int m0 = tile_m0(tile), n0 = tile_n0(tile);
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
@@ -375,7 +393,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
       // parity) and start the residual loads *before* waiting for the
       // accumulator: their latency hides under the main loop.
       float* vb = vecs + (local & 1) * (4 * BN);
-      for (int c = et; c < BN; c += EPI_THREADS) {
+      for (int c = et; c < (bias_all ? 0 : BN); c += EPI_THREADS) {
         vb[c] = ep.bias[n0 + c];
         if constexpr (KIND == EPI_RES) vb[BN + c] = ep.gate[(int64_t)slot * ep.vec_stride + n0 + c];
         if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
@@ -416,7 +434,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
         }
         __syncwarp();
       }
-      named_bar_sync(5, EPI_THREADS);  // vectors staged
+      if (!bias_all) named_bar_sync(5, EPI_THREADS);  // vectors staged
       if (warp == 2 && lane == 0) GTR(2, local);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -425,7 +443,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
         acc_release(acc);
         continue;
       }
-      const float* vbias = vb + c_lo;
+      const float* vbias = bias_all ? vecs + n0 + c_lo : vb + c_lo;
 
       if constexpr (KIND == EPI_F32) {
 #pragma unroll 1
@@ -472,11 +490,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
 #pragma unroll 1
         for (int c0 = 0; c0 < COLS; c0 += 64) {
           uint8_t* buf = out.acquire(lane);
+          if (warp == 2 && lane == 0) GTR(4, 3 * local + c0 / 64);
+#if SF_QKV_LD64
+          // both 32-column halves of the head in flight before one wait; the
+          // accumulator is released as soon as the tile's last columns are in registers
+          float v64[64];
+          tmem_ld32(taddr + c_lo + c0, *reinterpret_cast<float(*)[32]>(&v64[0]));
+          tmem_ld32(taddr + c_lo + c0 + 32, *reinterpret_cast<float(*)[32]>(&v64[32]));
+          tmem_ld_wait();
+          if (warp == 2 && lane == 0) GTR(5, 3 * local + c0 / 64);
+          if (c0 + 64 >= COLS) acc_release(acc);
+#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+#if SF_QKV_LD64
+            float* v = v64 + 32 * h;
+#else
             float v[32];
             tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
             tmem_ld_wait();
+#endif
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
@@ -601,11 +634,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           const int64_t hb = ((int64_t)slot * ep.heads + head);
           const float sc = which == 0 ? ep.q_scale : 1.0f;
           uint8_t* buf = out.acquire(lane);
+          if (warp == 2 && lane == 0) GTR(4, 3 * local + c0 / 64);
+#if SF_QKV_LD64
+          // both 32-column halves of the head in flight before one wait; the
+          // accumulator is released as soon as the tile's last columns are in registers
+          float v64[64];
+          tmem_ld32(taddr + c_lo + c0, *reinterpret_cast<float(*)[32]>(&v64[0]));
+          tmem_ld32(taddr + c_lo + c0 + 32, *reinterpret_cast<float(*)[32]>(&v64[32]));
+          tmem_ld_wait();
+          if (warp == 2 && lane == 0) GTR(5, 3 * local + c0 / 64);
+          if (c0 + 64 >= COLS) acc_release(acc);
+#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+#if SF_QKV_LD64
+            float* v = v64 + 32 * h;
+#else
             float v[32];
             tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
             tmem_ld_wait();
+#endif
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
@@ -628,13 +676,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
               }
             }
           }
-          if (c0 + 64 >= COLS) {
+          if (!SF_QKV_LD64 && c0 + 64 >= COLS) {
             acc_release(acc);
           }
+          if (warp == 2 && lane == 0) GTR(6, 3 * local + c0 / 64);
           if (which < 2 || SF_QKV_DIAG_NOVT)
             out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
           else
             out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
+          if (warp == 2 && lane == 0) GTR(7, 3 * local + c0 / 64);
         }
       } else if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
         // RES_LN: 12 epilogue warps; the 3 warps of a lane quarter split each
