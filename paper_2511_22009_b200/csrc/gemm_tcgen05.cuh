@@ -47,6 +47,9 @@ __device__ long long g_gemm_trace[8 * 64];
 #ifndef SF_QKV_NBUF
 #define SF_QKV_NBUF 3  // QKV epilogue: TMA-store staging buffers per warp (3: 118.7 vs 122.1 us, 4: 128.5 -- one A/B stage fewer)
 #endif
+#ifndef SF_QKV_VT_PAIR
+#define SF_QKV_VT_PAIR 1  // QKV epilogue: V^T staged as 4-byte token pairs (lane-pair shuffle)
+#endif
 #ifndef SF_QKV_LD64
 #define SF_QKV_LD64 1  // QKV epilogue: one TMEM-load wait per 64-column head chunk
 #endif
@@ -109,6 +112,9 @@ struct GemmCfg {
   static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;  // column offset between accumulator stages
   static constexpr int TMEM_COLS = ACC_STAGES == 2 ? (BN <= 128 ? 256 : 512) : (BN <= 256 ? 256 : 512);
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  // QKV with 8 epilogue warps: two 4-warp groups take alternate tiles (group g drains
+  // accumulator stage g) instead of splitting a tile's columns
+  static constexpr int TILE_GROUPS = (KIND == EPI_QKV && BN == 192 && EPI_WARPS == 8) ? 2 : 1;
   static constexpr int RED_BYTES = 2 * EPI_WARPS * 32 * 4;  // LN partial sums of the warps sharing a row
   static constexpr int VEC_BYTES = 2 * 4 * BN * 4;          // per-tile column vectors, double-buffered
   // per-warp output staging, double-buffered: 32 rows x 128 B (SW128), or 32 x 64 B (SW64) with 12 warps
@@ -132,6 +138,7 @@ struct GemmCfg {
   static_assert(MMA_N % 16 == 0 && MMA_N <= 256, "bad MMA N");
   static_assert(B_BOX <= 256, "bad box");
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8 || EPI_WARPS == 12 || EPI_WARPS == 16, "epilogue warps");
+  static_assert(TILE_GROUPS == 1 || ACC_STAGES == 2, "tile groups drain one accumulator stage each");
 };
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     }
     for (int a = 0; a < C::ACC_STAGES; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CTAS * EPI_WARPS * 32);
+      mbar_init(&tempty[a], CTAS * EPI_WARPS * 32 / C::TILE_GROUPS);
     }
     if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES || KIND == EPI_RES_LN2)
       for (int i = 0; i < EPI_WARPS * 4; ++i) mbar_init(&rbar[i], 1);
@@ -365,8 +372,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     const uint32_t e = warp - 2;
     const uint32_t quarter = warp & 3;
     constexpr int EPI_THREADS = EPI_WARPS * 32;
-    constexpr int COLS = BN / (EPI_WARPS / 4);  // columns per thread (warps sharing a lane quarter split them)
-    const int c_lo = (int)(e / 4) * COLS;
+    constexpr int COLS = BN / (EPI_WARPS / 4 / C::TILE_GROUPS);  // columns per thread (warps sharing a lane quarter split them)
+    const int c_lo = C::TILE_GROUPS > 1 ? 0 : (int)(e / 4) * COLS;
+    const uint32_t tgroup = C::TILE_GROUPS > 1 ? e / 4 : 0;
     const int et = threadIdx.x - 64;
     using OutStage = OutStageT<C::OUT_BUF, C::LN_RING ? 2 : C::OUT_NBUF>;
     OutStage out{sOut + e * C::OUT_NBUF * C::OUT_BUF, 0};
@@ -382,6 +390,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
       named_bar_sync(5, EPI_THREADS);
     }
     for (int tile = t_first; tile < t_limit; tile += t_stride, ++local) {
+      if (C::TILE_GROUPS > 1 && (local & 1) != tgroup) continue;  // the other group's tile
       const int m0 = tile_m0(tile), n0 = tile_n0(tile);
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       const int r0 = m0 + quarter * 32;  // first row of this warp
@@ -434,7 +443,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
         }
         __syncwarp();
       }
-      if (!bias_all) named_bar_sync(5, EPI_THREADS);  // vectors staged
+      if (!bias_all)  // vectors staged (tile groups: per group)
+        named_bar_sync(C::TILE_GROUPS > 1 ? 6 + tgroup : 5, EPI_THREADS / C::TILE_GROUPS);
       if (warp == 2 && lane == 0) GTR(2, local);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -668,12 +678,29 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
             } else {
               // V^T staging: 64 rows (head dim) x 64 B (32 tokens), 64B swizzle:
               // 16-byte chunk c of row dd lives at chunk c ^ ((dd >> 1) & 3)
+#if SF_QKV_VT_PAIR
+              // dims (2p, 2p+1) x tokens (2j, 2j+1) are swapped across lane pairs with one
+              // shuffle, so each lane stores a 4-byte token pair: 16 STS.32 (1 wavefront
+              // each: the two rows are adjacent 64-byte halves) instead of 32 STS.16
+              const uint32_t odd = lane & 1;
+#pragma unroll
+              for (int pi = 0; pi < 16; ++pi) {
+                uint32_t own;
+                asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(own) : "f"(v[2 * pi + 1]), "f"(v[2 * pi]));
+                const uint32_t other = __shfl_xor_sync(0xffffffffu, own, 1);
+                const uint32_t w = __byte_perm(own, other, odd ? 0x3276 : 0x5410);
+                const uint32_t dd = 32 * h + 2 * pi + odd;
+                *reinterpret_cast<uint32_t*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
+                                             (lane & 6) * 2) = w;  // V^T is fp16 (PV runs in fp16)
+              }
+#else
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const uint32_t dd = 32 * h + i;
                 *reinterpret_cast<__half*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
                                            (lane & 7) * 2) = __float2half_rn(v[i]);  // V^T is fp16 (PV runs in fp16)
               }
+#endif
             }
           }
           if (!SF_QKV_LD64 && c0 + 64 >= COLS) {
