@@ -18,6 +18,10 @@
 #include "gemm_tcgen05.cuh"
 #include "sf_internal.h"
 
+#ifndef SF_FINAL_MMA
+#define SF_FINAL_MMA 1  // final layer on mma.sync (0: the per-lane FMA kernel)
+#endif
+
 namespace sf {
 
 // ============================================================ shared helpers
@@ -334,6 +338,85 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
+// 16-byte streaming load (read once: no L1 allocation)
+__device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// d += A(16x16 bf16) * B(16x8 bf16), fp32 accumulate (warp-level tensor path)
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Output side of the final layer, shared by the FMA and the mma.sync kernels.
+struct FinalOut {
+  int HW, P, C;
+  float* eps_out;      // direct mode
+  const int64_t* ctl;  // stream mode from here on
+  int n;
+  int64_t m;
+  const double* stage_params;
+  const int64_t* row_info;
+  float* x_ring;
+  const float* noise_in;
+  uint64_t noise_seed;
+  float* frames_out;
+  int64_t* frame_ids;
+};
+
+// eps of feature f of token tau of latent row lr -> unpatchify, then either store it
+// (direct) or apply the Euler step + emit + refill of that latent element (stream).
+template <bool STREAM>
+__device__ __forceinline__ void final_element(const FinalOut& o, int64_t j, int64_t lr, int tau, int gw, int f, float e) {
+  const int HW = o.HW, P = o.P, C = o.C;
+  const int64_t D = (int64_t)C * HW * HW;
+  const int pi = tau / gw, pj = tau % gw;
+  // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
+  const int c = f % C, q = (f / C) % P, p = f / (C * P);
+  const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
+  if constexpr (!STREAM) {
+    o.eps_out[lr * D + idx] = e;
+  } else {
+    const int n = o.n;
+    const int64_t stage = o.row_info[lr * 4 + 0];
+    const int64_t g = o.row_info[lr * 4 + 1];
+    const bool active = o.row_info[lr * 4 + 2] != 0;
+    const int64_t s = o.row_info[lr * 4 + 3];
+    const int64_t k = lr % n;
+    const bool refill_slot = (k == (j + 1) % n);
+    const bool admit = refill_slot && (j + 1 < o.m);
+    const bool retiring = active && (stage + 1 == n);
+    if (refill_slot && tau == 0 && f == 0) o.frame_ids[s] = retiring ? g : -1;
+    float* xr = o.x_ring + lr * D;
+    const float noise =
+        admit ? (o.noise_in ? o.noise_in[s * D + idx] : philox_normal(o.noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
+    if (active) {
+      const double* pp = o.stage_params + stage * SF_PARAM_STRIDE;
+      const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
+      const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
+      const bool at_end = pp[SF_P_AT_END] != 0.0;
+      const float xo = xr[idx];
+      // velocity.py:125-130 in fp32
+      const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
+      const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
+      const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
+      if (retiring) o.frames_out[s * D + idx] = xn;
+      xr[idx] = admit ? noise : xn;
+    } else if (admit) {
+      xr[idx] = noise;
+    }
+  }
+}
+
 // One warp per group of 4 consecutive tokens (grid-stride).  Lane partial dot
 // products over its 4 x U columns for all 4 tokens x 16 output features (each
 // float4 weight read serves the 4 tokens), then a butterfly reduce-scatter
@@ -426,46 +509,115 @@ __global__ void __launch_bounds__(256) final_layer_kernel(
       }
     }
     const int tau = tau0 + my_t;
-    const int pi = tau / gw, pj = tau % gw;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int f = my_f + h;
-      const float e = h ? e2.y : e2.x;
-      // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
-      const int c = f % C, q = (f / C) % P, p = f / (C * P);
-      const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
-      if constexpr (!STREAM) {
-        eps_out[lr * D + idx] = e;
-      } else {
-        const int64_t stage = row_info[lr * 4 + 0];
-        const int64_t g = row_info[lr * 4 + 1];
-        const bool active = row_info[lr * 4 + 2] != 0;
-        const int64_t s = row_info[lr * 4 + 3];
-        const int64_t k = lr % n;
-        const bool refill_slot = (k == (j + 1) % n);
-        const bool admit = refill_slot && (j + 1 < m);
-        const bool retiring = active && (stage + 1 == n);
-        if (refill_slot && tau == 0 && f == 0) frame_ids[s] = retiring ? g : -1;
-        float* xr = x_ring + lr * D;
-        const float noise =
-            admit ? (noise_in ? noise_in[s * D + idx] : philox_normal(noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
-        if (active) {
-          const double* pp = stage_params + stage * SF_PARAM_STRIDE;
-          const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
-          const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
-          const bool at_end = pp[SF_P_AT_END] != 0.0;
-          const float xo = xr[idx];
-          // velocity.py:125-130 in fp32
-          const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
-          const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
-          const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
-          if (retiring) frames_out[s * D + idx] = xn;
-          xr[idx] = admit ? noise : xn;
-        } else if (admit) {
-          xr[idx] = noise;
-        }
+    for (int h = 0; h < 2; ++h)
+      final_element<STREAM>(FinalOut{HW, P, C, eps_out, ctl, n, m, stage_params, row_info, x_ring, noise_in,
+                                     noise_seed, frames_out, frame_ids},
+                            j, lr, tau, gw, my_f + h, h ? e2.y : e2.x);
+  }
+}
+
+// Same layer on the warp-level tensor path (mma.sync m16n8k16, bf16 in, fp32
+// accumulate): one warp per 16 consecutive tokens (T % 16 == 0), N = 16 output
+// features as two n8 tiles, K = HID in 16-wide steps.  The projection is ~0.4% of the
+// network's FLOPs, so the legacy HMMA rate is ample; what matters is that xmod
+// (the kernel's only large input, T*HID bf16 per row) streams at HBM rate: each
+// lane reads 16-byte runs, K permuted so that a lane's run feeds its own fragments
+// (logical k {2c, 2c+1, 2c+8, 2c+9} of a 16-step <-> physical 8c + {0, 1, 2, 3},
+// the same map for A and B, so the dot products are unchanged).  Fragment
+// ownership after the MMA: lane (g = lane/4, c = lane%4) holds tokens g and g+8,
+// features {2c, 2c+1} and {8+2c, 9+2c}.
+constexpr int FINAL_WPAD = 64;  // bytes of padding per smem weight row (conflict-free LDS.128)
+
+template <int HID, bool STREAM>
+__global__ void __launch_bounds__(256) final_layer_mma_kernel(
+    const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
+    int P, int C, int64_t lat_rows, float* __restrict__ eps_out, const int64_t* __restrict__ ctl, int n, int64_t m,
+    const double* __restrict__ stage_params, const int64_t* __restrict__ row_info, int cfg, float w,
+    float* __restrict__ x_ring, const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
+    int64_t* __restrict__ frame_ids, int64_t total_tokens) {
+  constexpr int PK = 16;
+  constexpr int WROW = HID * 2 + FINAL_WPAD;  // bytes
+  extern __shared__ __align__(16) uint8_t fsm[];  // [PK][WROW] bf16 weights, then bias[PK]
+  float* sbias = reinterpret_cast<float*>(fsm + PK * WROW);
+  for (int idx = threadIdx.x; idx < PK * HID / 8; idx += blockDim.x) {
+    const int r = idx / (HID / 8), c8 = idx % (HID / 8);
+    *reinterpret_cast<uint4*>(fsm + r * WROW + c8 * 16) = reinterpret_cast<const uint4*>(fw)[idx];
+  }
+  if (threadIdx.x < PK) sbias[threadIdx.x] = fb[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  const int gw = HW / P, T = gw * gw;
+  int64_t j = 0;
+  if constexpr (STREAM) j = ctl[1];
+  const uint8_t* wrow0 = fsm + g * WROW + 16 * c;        // feature g      (n-tile 0)
+  const uint8_t* wrow1 = fsm + (g + 8) * WROW + 16 * c;  // feature g + 8  (n-tile 1)
+
+  // acc[nt][0..1]: token g, features 8nt + 2c + {0,1}; acc[nt][2..3]: token g + 8
+  auto project = [&](int64_t net_row, int tau0, float (&acc)[2][4]) {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
+    const uint8_t* a0 = reinterpret_cast<const uint8_t*>(xmod + (net_row * T + tau0 + g) * HID) + 16 * c;
+    const uint8_t* a1 = a0 + 8 * HID * 2;
+    constexpr int NCH = HID / 32;  // 32 K elements (two k-steps) per 16-byte lane run
+    constexpr int UNR = 6;
+    static_assert(NCH % UNR == 0, "chunking");
+#pragma unroll 1
+    for (int ch0 = 0; ch0 < NCH; ch0 += UNR) {
+      uint4 xa[UNR], xb[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        xa[u] = ldg_stream_u4(a0 + 64 * (ch0 + u));
+        xb[u] = ldg_stream_u4(a1 + 64 * (ch0 + u));
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint4 b0 = *reinterpret_cast<const uint4*>(wrow0 + 64 * (ch0 + u));
+        const uint4 b1 = *reinterpret_cast<const uint4*>(wrow1 + 64 * (ch0 + u));
+        mma_bf16_16816(acc[0], xa[u].x, xb[u].x, xa[u].y, xb[u].y, b0.x, b0.y);
+        mma_bf16_16816(acc[1], xa[u].x, xb[u].x, xa[u].y, xb[u].y, b1.x, b1.y);
+        mma_bf16_16816(acc[0], xa[u].z, xb[u].z, xa[u].w, xb[u].w, b0.z, b0.w);
+        mma_bf16_16816(acc[1], xa[u].z, xb[u].z, xa[u].w, xb[u].w, b1.z, b1.w);
       }
     }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const float bl = sbias[8 * nt + 2 * c], bh = sbias[8 * nt + 2 * c + 1];
+      acc[nt][0] += bl;
+      acc[nt][1] += bh;
+      acc[nt][2] += bl;
+      acc[nt][3] += bh;
+    }
+  };
+
+  const FinalOut o{HW, P, C, eps_out, ctl, n, m, stage_params, row_info, x_ring, noise_in, noise_seed, frames_out,
+                   frame_ids};
+  const int64_t groups = total_tokens / 16;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
+    const int64_t tok0 = grp * 16;
+    const int64_t lr = tok0 / T;
+    const int tau0 = (int)(tok0 % T);
+    float e[2][4];
+    project(STREAM && cfg ? lr + lat_rows : lr, tau0, e);
+    if constexpr (STREAM) {
+      if (cfg) {
+        float eu[2][4];
+        project(lr, tau0, eu);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)  // handle_cfg (models.py:288-293)
+            e[nt][i] = __fadd_rn(eu[nt][i], __fmul_rn(w, __fsub_rn(e[nt][i], eu[nt][i])));
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        final_element<STREAM>(o, j, lr, tau0 + g + 8 * (i >> 1), gw, 8 * nt + 2 * c + (i & 1), e[nt][i]);
   }
 }
 
@@ -743,6 +895,29 @@ static size_t final_smem(const sf_dit_config& c) {
   return (size_t)(PK * c.hidden + PK) * sizeof(float);
 }
 
+// Final layer + Euler/emit/refill: the mma.sync kernel (default) or the FMA kernel (SF_FINAL_MMA=0).
+template <bool STREAM>
+static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int64_t* ctl, int n, int64_t m,
+                         const double* stage_params, const int64_t* row_info, int cfg, float w, float* x_ring,
+                         const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                         int64_t tokens, cudaStream_t st) {
+  const sf_dit_config& c = h->cfg;
+  const __nv_bfloat16* fw = (const __nv_bfloat16*)h->w.final_w;
+#if SF_FINAL_MMA
+  const int PK = c.in_ch * c.patch * c.patch;
+  const size_t sm = (size_t)PK * (c.hidden * 2 + FINAL_WPAD) + PK * sizeof(float);
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + 7) / 8, 148 * 8);
+  auto fk = c.hidden == 384 ? final_layer_mma_kernel<384, STREAM> : final_layer_mma_kernel<1152, STREAM>;
+#else
+  const size_t sm = final_smem(c);
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8);
+  auto fk = c.hidden == 384 ? final_layer_kernel<384, STREAM> : final_layer_kernel<1152, STREAM>;
+#endif
+  fk<<<blocks, 256, sm, st>>>(h->xmod, fw, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
+                              stage_params, row_info, cfg, w, x_ring, noise_in, noise_seed, frames_out, frame_ids,
+                              tokens);
+}
+
 extern "C" {
 
 int64_t sf_dit_workspace_bytes(const sf_dit_config* cfg, int64_t max_rows) {
@@ -853,10 +1028,8 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if ((rc = launch_patch(h, x, rows, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = rows * h->tokens;
-  auto fk = c.hidden == 384 ? final_layer_kernel<384, false> : final_layer_kernel<1152, false>;
-  fk<<<(unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8), 256, final_smem(c), st>>>(
-      h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, rows, eps_out,
-      nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr, tokens);
+  launch_final<false>(h, rows, eps_out, nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr,
+                      tokens, st);
   return cuda_status();
 }
 
@@ -877,10 +1050,8 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = R * h->tokens;
-  auto fk = c.hidden == 384 ? final_layer_kernel<384, true> : final_layer_kernel<1152, true>;
-  fk<<<(unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8), 256, final_smem(c), st>>>(
-      h->xmod, (const __nv_bfloat16*)h->w.final_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, R, nullptr, ctl, n,
-      m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed, frames_out, frame_ids, tokens);
+  launch_final<true>(h, R, nullptr, ctl, n, m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed,
+                     frames_out, frame_ids, tokens, st);
   mark(h, P_FINAL, st);
   return cuda_status();
 }
