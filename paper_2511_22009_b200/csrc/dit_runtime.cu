@@ -21,6 +21,9 @@
 #ifndef SF_FINAL_MMA
 #define SF_FINAL_MMA 1  // final layer on mma.sync (0: the per-lane FMA kernel)
 #endif
+#ifndef SF_PATCH_MMA
+#define SF_PATCH_MMA 1  // patch embed + LN1 on mma.sync (0: the per-lane FMA kernel)
+#endif
 
 namespace sf {
 
@@ -154,6 +157,25 @@ __global__ void __launch_bounds__(256) cond_out_kernel(RowSrc src, int hidden, c
   }
 }
 
+// 16-byte streaming load (read once: no L1 allocation)
+__device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// d += A(16x16 bf16) * B(16x8 bf16), fp32 accumulate (warp-level tensor path)
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 // ============================================================ K2+K4: patch embed + pos + LN1 modulate
 // One warp per group of TOK consecutive tokens (grid-stride); lane owns columns
 // 128u + 4 lane + {0..3}.  Weights live in smem transposed ([PK][HID]); each
@@ -271,6 +293,152 @@ __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
   }
 }
 
+// The same patch embed + LN1 modulate on the warp-level tensor path (mma.sync
+// m16n8k16): one warp per 16 consecutive tokens, K = 16 = the patch vector
+// (C=4, P=2), HID/8 n8 tiles.  x is fp32, so it enters as a bf16 hi/lo pair
+// (x = hi + lo to 2^-17 relative; two MMAs per tile) against the bf16 weights,
+// fp32 accumulate: the sum matches the FMA kernel to fp32 rounding.  Lane (g =
+// lane/4, c = lane%4) holds A pairs k = 2c, 2c+1 (channel c/2, patch row c%2: one
+// float2 of x) and k = 2c+8, 2c+9 (channel c/2 + 2), and after each MMA tokens g,
+// g+8 x fragment columns 2c, 2c+1 of each tile.  Output columns are permuted over
+// blocks of four tiles: fragment column 2c+e of tile q of block blk is hidden column
+// 32 blk + 8c + 2q + e, so a lane owns 8 consecutive columns per block (one 16-byte
+// bf16 run, two float4 of pos).  The B fragments (weight rows in that order) are
+// pre-arranged in smem as one uint2 per lane per tile (conflict-free LDS.64).  The
+// 16 residual rows (one contiguous 16*HID bf16 block in HBM) are staged in a padded
+// smem tile (row stride HID*2 + 64 B: a quarter-warp's 16-byte writes hit 32
+// distinct banks) with their row statistics, then written out as 16-byte coalesced
+// stores, and LN + modulate runs in that copy-out layout from the staged bf16
+// residual (no second projection).
+template <int HID>
+struct PatchMma {
+  static constexpr int NT = HID / 8;
+  static constexpr int WARPS = HID <= 384 ? 7 : 4;  // two CTAs per SM at hidden 384 (smem)
+  static constexpr int ROW = HID * 2 + 64;                 // staged row stride, bytes
+  static constexpr int WBUF = 16 * ROW + 16 * 2 * 4;       // per warp: 16 rows + (mean, rstd) x 16
+  static constexpr int SMEM = NT * 32 * 8 + HID * 4 + WARPS * WBUF;  // B fragments, bias, per-warp buffers
+};
+
+template <int HID>
+__global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_kernel(
+    const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
+    const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
+    float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
+  using PM = PatchMma<HID>;
+  constexpr int NT = PM::NT, ROW = PM::ROW;
+  extern __shared__ __align__(16) uint8_t psm[];
+  uint2* sB = reinterpret_cast<uint2*>(psm);  // [NT][32 lanes]
+  const uint32_t* pw32 = reinterpret_cast<const uint32_t*>(pw);  // [HID][8] bf16 pairs
+  float* sBias = reinterpret_cast<float*>(psm + NT * 32 * 8);
+  for (int idx = threadIdx.x; idx < NT * 32; idx += blockDim.x) {
+    const int tile = idx / 32, gg = (idx % 32) / 4, cc = idx % 4;
+    const int n = 32 * (tile / 4) + 8 * (gg >> 1) + 2 * (tile % 4) + (gg & 1);  // permuted weight row
+    sB[idx] = make_uint2(pw32[n * 8 + cc], pw32[n * 8 + 4 + cc]);
+  }
+  for (int idx = threadIdx.x; idx < HID; idx += blockDim.x) sBias[idx] = pb[idx];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  uint8_t* sY = psm + NT * 32 * 8 + HID * 4 + warp * PM::WBUF;  // [16][ROW] staged bf16 residual rows
+  float* sStat = reinterpret_cast<float*>(sY + 16 * ROW);      // [16][mean, rstd]
+  const int gw = HW / P, T = gw * gw;
+  const int64_t groups = total_tokens / 16;
+  const int64_t wstride = (int64_t)gridDim.x * PM::WARPS;
+  for (int64_t grp = (int64_t)blockIdx.x * PM::WARPS + warp; grp < groups; grp += wstride) {
+    const int64_t tok0 = grp * 16;
+    const int64_t ni = tok0 / T;
+    const int tau0 = (int)(tok0 % T);
+    const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
+    uint32_t ahi[4], alo[4];  // A registers: (row g, k 2c) (row g+8, k 2c) (row g, k 2c+8) (row g+8, k 2c+8)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int tau = tau0 + g + 8 * (i & 1);
+      const int pi = tau / gw, pj = tau % gw;
+      const int ch = (c >> 1) + 2 * (i >> 1), p = c & 1;
+      const float2 v = __ldg(reinterpret_cast<const float2*>(xl + (int64_t)ch * HW * HW + (pi * 2 + p) * HW + pj * 2));
+      ahi[i] = pack_bf16(v.x, v.y);
+      const float2 h = unpack_bf16(ahi[i]);
+      alo[i] = pack_bf16(v.x - h.x, v.y - h.y);
+    }
+    const float* pos0 = pos + (int64_t)(tau0 + g) * HID + 8 * c;
+    const float* pos1 = pos0 + 8 * HID;
+    uint8_t* y0 = sY + g * ROW + 16 * c;
+    uint8_t* y1 = y0 + 8 * ROW;
+    float sum0 = 0.f, sum1 = 0.f, sq0 = 0.f, sq1 = 0.f;
+#pragma unroll 2
+    for (int blk = 0; blk < HID / 32; ++blk) {
+      float acc[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint2 b = sB[(4 * blk + q) * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[q][i] = 0.f;
+        mma_bf16_16816(acc[q], ahi[0], ahi[1], ahi[2], ahi[3], b.x, b.y);
+        mma_bf16_16816(acc[q], alo[0], alo[1], alo[2], alo[3], b.x, b.y);
+      }
+      // lane columns 32 blk + 8c + {0..7}: column 2q + e <- acc[q][e] (row g), acc[q][2 + e] (row g+8)
+      float pb0[8], pb1[8], bias[8];
+      *reinterpret_cast<float4*>(&pb0[0]) = __ldg(reinterpret_cast<const float4*>(pos0 + 32 * blk));
+      *reinterpret_cast<float4*>(&pb0[4]) = __ldg(reinterpret_cast<const float4*>(pos0 + 32 * blk + 4));
+      *reinterpret_cast<float4*>(&pb1[0]) = __ldg(reinterpret_cast<const float4*>(pos1 + 32 * blk));
+      *reinterpret_cast<float4*>(&pb1[4]) = __ldg(reinterpret_cast<const float4*>(pos1 + 32 * blk + 4));
+      *reinterpret_cast<float4*>(&bias[0]) = *reinterpret_cast<const float4*>(sBias + 32 * blk + 8 * c);
+      *reinterpret_cast<float4*>(&bias[4]) = *reinterpret_cast<const float4*>(sBias + 32 * blk + 8 * c + 4);
+      uint32_t r0[4], r1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // residual, stored bf16 (bias + pos first, as the FMA kernel)
+        r0[q] = pack_bf16(acc[q][0] + (bias[2 * q] + pb0[2 * q]), acc[q][1] + (bias[2 * q + 1] + pb0[2 * q + 1]));
+        r1[q] = pack_bf16(acc[q][2] + (bias[2 * q] + pb1[2 * q]), acc[q][3] + (bias[2 * q + 1] + pb1[2 * q + 1]));
+        const float2 f0 = unpack_bf16(r0[q]), f1 = unpack_bf16(r1[q]);
+        sum0 += f0.x + f0.y;
+        sum1 += f1.x + f1.y;
+        sq0 += f0.x * f0.x + f0.y * f0.y;
+        sq1 += f1.x * f1.x + f1.y * f1.y;
+      }
+      *reinterpret_cast<uint4*>(y0 + 64 * blk) = make_uint4(r0[0], r0[1], r0[2], r0[3]);
+      *reinterpret_cast<uint4*>(y1 + 64 * blk) = make_uint4(r1[0], r1[1], r1[2], r1[3]);
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      sum0 += __shfl_xor_sync(0xffffffffu, sum0, o);
+      sum1 += __shfl_xor_sync(0xffffffffu, sum1, o);
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, o);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, o);
+    }
+    if (c == 0) {
+      const float mean0 = sum0 / HID, mean1 = sum1 / HID;
+      sStat[2 * g] = mean0;
+      sStat[2 * g + 1] = rsqrtf(fmaxf(sq0 / HID - mean0 * mean0, 0.f) + ln_eps);
+      sStat[2 * (g + 8)] = mean1;
+      sStat[2 * (g + 8) + 1] = rsqrtf(fmaxf(sq1 / HID - mean1 * mean1, 0.f) + ln_eps);
+    }
+    __syncwarp();
+    // copy-out: 16 B (8 columns of one row) per lane; LN + modulate on the same 8 values
+    const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
+    const float* scale = shift + HID;
+    constexpr int CPR = HID / 8;  // 16-byte chunks per row
+#pragma unroll 4
+    for (int idx = lane; idx < 16 * CPR; idx += 32) {
+      const int row = idx / CPR, k = idx % CPR;
+      const uint4 v = *reinterpret_cast<const uint4*>(sY + row * ROW + 16 * k);
+      const int64_t off = (tok0 + row) * HID + 8 * k;
+      *reinterpret_cast<uint4*>(xres + off) = v;
+      const float mean = sStat[2 * row], rstd = sStat[2 * row + 1];
+      const float4 sh0 = __ldg(reinterpret_cast<const float4*>(shift + 8 * k));
+      const float4 sh1 = __ldg(reinterpret_cast<const float4*>(shift + 8 * k + 4));
+      const float4 sc0 = __ldg(reinterpret_cast<const float4*>(scale + 8 * k));
+      const float4 sc1 = __ldg(reinterpret_cast<const float4*>(scale + 8 * k + 4));
+      const float2 a = unpack_bf16(v.x), b = unpack_bf16(v.y), cc = unpack_bf16(v.z), d = unpack_bf16(v.w);
+      uint4 o;
+      o.x = pack_bf16((a.x - mean) * rstd * (1.0f + sc0.x) + sh0.x, (a.y - mean) * rstd * (1.0f + sc0.y) + sh0.y);
+      o.y = pack_bf16((b.x - mean) * rstd * (1.0f + sc0.z) + sh0.z, (b.y - mean) * rstd * (1.0f + sc0.w) + sh0.w);
+      o.z = pack_bf16((cc.x - mean) * rstd * (1.0f + sc1.x) + sh1.x, (cc.y - mean) * rstd * (1.0f + sc1.y) + sh1.y);
+      o.w = pack_bf16((d.x - mean) * rstd * (1.0f + sc1.z) + sh1.z, (d.y - mean) * rstd * (1.0f + sc1.w) + sh1.w);
+      *reinterpret_cast<uint4*>(xmod + off) = o;
+    }
+    __syncwarp();  // staged rows consumed before the next group overwrites them
+  }
+}
+
 // ============================================================ K4: LayerNorm + adaLN modulate (wide rows)
 // xmod = LN(xres) * (1 + scale[slot]) + shift[slot]; one warp per token, lane
 // owns columns 128u + 4 lane + {0..3}.  Used where the row is wider than one
@@ -338,25 +506,6 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
-// 16-byte streaming load (read once: no L1 allocation)
-__device__ __forceinline__ uint4 ldg_stream_u4(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// d += A(16x16 bf16) * B(16x8 bf16), fp32 accumulate (warp-level tensor path)
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                               uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
 // Output side of the final layer, shared by the FMA and the mma.sync kernels.
 struct FinalOut {
   int HW, P, C;
@@ -881,10 +1030,18 @@ static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t 
 static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const int64_t tokens = rows * h->tokens;
+#if SF_PATCH_MMA
+  const size_t sm = c.hidden == 384 ? PatchMma<384>::SMEM : PatchMma<1152>::SMEM;
+  const int wpb = c.hidden == 384 ? PatchMma<384>::WARPS : PatchMma<1152>::WARPS;
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, 148 * 8);
+  auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
+#else
   const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8);
   auto kern = c.hidden == 384 ? patch_embed_ln_kernel<384> : patch_embed_ln_kernel<1152>;
-  kern<<<blocks, 256, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
+  const int wpb = 8;
+#endif
+  kern<<<blocks, 32 * wpb, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
                                 h->w.patch_b, h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens);
   mark(h, P_PATCH, st);
   return cuda_status();
@@ -1000,6 +1157,10 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
   const int psm = (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)), fsm = (int)final_smem(c);
   cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
   cudaFuncSetAttribute(patch_embed_ln_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+  cudaFuncSetAttribute(patch_embed_ln_mma_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       PatchMma<384>::SMEM);
+  cudaFuncSetAttribute(patch_embed_ln_mma_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       PatchMma<1152>::SMEM);
   cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   cudaFuncSetAttribute(final_layer_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   cudaFuncSetAttribute(final_layer_kernel<1152, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
