@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(256) patch_embed_ln_kernel(
 // pre-arranged in smem as one uint2 per lane per tile (conflict-free LDS.64).  The
 // 16 residual rows (one contiguous 16*HID bf16 block in HBM) are staged in a padded
 // smem tile (row stride HID*2 + 64 B: a quarter-warp's 16-byte writes hit 32
-// distinct banks) with their row statistics, then written out as 16-byte coalesced
-// stores, and LN + modulate runs in that copy-out layout from the staged bf16
+// distinct banks) with their row statistics, then written out as coalesced 256-byte
+// warp stores, and LN + modulate runs in that copy-out layout from the staged bf16
 // residual (no second projection).
 template <int HID>
 struct PatchMma {
@@ -412,28 +412,34 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
       sStat[2 * (g + 8) + 1] = rsqrtf(fmaxf(sq1 / HID - mean1 * mean1, 0.f) + ln_eps);
     }
     __syncwarp();
-    // copy-out: 16 B (8 columns of one row) per lane; LN + modulate on the same 8 values
+    // copy-out: 8 B (4 columns) per lane and row, each lane on fixed columns 4k, k = lane + 32j, so the
+    // slot's shift/scale for them are loaded once per group; LN + modulate on the staged bf16 residual
     const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
     const float* scale = shift + HID;
-    constexpr int CPR = HID / 8;  // 16-byte chunks per row
-#pragma unroll 4
-    for (int idx = lane; idx < 16 * CPR; idx += 32) {
-      const int row = idx / CPR, k = idx % CPR;
-      const uint4 v = *reinterpret_cast<const uint4*>(sY + row * ROW + 16 * k);
-      const int64_t off = (tok0 + row) * HID + 8 * k;
-      *reinterpret_cast<uint4*>(xres + off) = v;
+    constexpr int J = HID / 128;
+    float4 sh[J], sc[J];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      sh[jj] = __ldg(reinterpret_cast<const float4*>(shift + 4 * (lane + 32 * jj)));
+      sc[jj] = __ldg(reinterpret_cast<const float4*>(scale + 4 * (lane + 32 * jj)));
+    }
+#pragma unroll 2
+    for (int row = 0; row < 16; ++row) {
       const float mean = sStat[2 * row], rstd = sStat[2 * row + 1];
-      const float4 sh0 = __ldg(reinterpret_cast<const float4*>(shift + 8 * k));
-      const float4 sh1 = __ldg(reinterpret_cast<const float4*>(shift + 8 * k + 4));
-      const float4 sc0 = __ldg(reinterpret_cast<const float4*>(scale + 8 * k));
-      const float4 sc1 = __ldg(reinterpret_cast<const float4*>(scale + 8 * k + 4));
-      const float2 a = unpack_bf16(v.x), b = unpack_bf16(v.y), cc = unpack_bf16(v.z), d = unpack_bf16(v.w);
-      uint4 o;
-      o.x = pack_bf16((a.x - mean) * rstd * (1.0f + sc0.x) + sh0.x, (a.y - mean) * rstd * (1.0f + sc0.y) + sh0.y);
-      o.y = pack_bf16((b.x - mean) * rstd * (1.0f + sc0.z) + sh0.z, (b.y - mean) * rstd * (1.0f + sc0.w) + sh0.w);
-      o.z = pack_bf16((cc.x - mean) * rstd * (1.0f + sc1.x) + sh1.x, (cc.y - mean) * rstd * (1.0f + sc1.y) + sh1.y);
-      o.w = pack_bf16((d.x - mean) * rstd * (1.0f + sc1.z) + sh1.z, (d.y - mean) * rstd * (1.0f + sc1.w) + sh1.w);
-      *reinterpret_cast<uint4*>(xmod + off) = o;
+#pragma unroll
+      for (int jj = 0; jj < J; ++jj) {
+        const int k = lane + 32 * jj;
+        const uint2 v = *reinterpret_cast<const uint2*>(sY + row * ROW + 8 * k);
+        const int64_t off = (tok0 + row) * HID + 4 * k;
+        *reinterpret_cast<uint2*>(xres + off) = v;
+        const float2 a = unpack_bf16(v.x), b = unpack_bf16(v.y);
+        uint2 o;
+        o.x = pack_bf16((a.x - mean) * rstd * (1.0f + sc[jj].x) + sh[jj].x,
+                        (a.y - mean) * rstd * (1.0f + sc[jj].y) + sh[jj].y);
+        o.y = pack_bf16((b.x - mean) * rstd * (1.0f + sc[jj].z) + sh[jj].z,
+                        (b.y - mean) * rstd * (1.0f + sc[jj].w) + sh[jj].w);
+        *reinterpret_cast<uint2*>(xmod + off) = o;
+      }
     }
     __syncwarp();  // staged rows consumed before the next group overwrites them
   }
