@@ -1039,7 +1039,9 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
 #if SF_PATCH_MMA
   const size_t sm = c.hidden == 384 ? PatchMma<384>::SMEM : PatchMma<1152>::SMEM;
   const int wpb = c.hidden == 384 ? PatchMma<384>::WARPS : PatchMma<1152>::WARPS;
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, 148 * 8);
+  // persistent: as many CTAs as fit (smem-limited: 2 per SM at hidden 384, 1 at 1152), each warp
+  // walks several 16-token groups, so the B-fragment fill is paid once per CTA
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, c.hidden == 384 ? 2 * 148 : 148);
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
 #else
   const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
