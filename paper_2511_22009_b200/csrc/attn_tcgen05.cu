@@ -55,6 +55,9 @@
 #ifndef SF_ATTN_MAX3
 #define SF_ATTN_MAX3 1  // row max as four 3-input max chains (32+2 FMNMX3) instead of 8 + 24 + 7 (276.4 vs 279.9 us)
 #endif
+#ifndef SF_ATTN_KV_STAGES
+#define SF_ATTN_KV_STAGES 6  // K/V^T ring depth (64-key stages of 18 KB at head dim 64)
+#endif
 #ifndef SF_ATTN_EMU_PAIRS
 #define SF_ATTN_EMU_PAIRS 6  // exp2 pairs per 32-key chunk evaluated by polynomial (of 16)
 #endif
@@ -76,7 +79,7 @@ __device__ long long g_attn_trace[16 * 64];
 namespace attn {
 constexpr int BQ = 128;  // queries per tile (2 tiles per item)
 constexpr int BKV = 64;  // keys per KV tile
-constexpr int KV_STAGES = 6;
+constexpr int KV_STAGES = SF_ATTN_KV_STAGES;
 constexpr int QBUF = 2;
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int TMEM_COLS = 512;
