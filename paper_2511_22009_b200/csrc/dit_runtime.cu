@@ -610,7 +610,6 @@ __global__ void __launch_bounds__(256) final_layer_kernel(
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int gw = HW / P, T = gw * gw;
-  const int64_t D = (int64_t)C * HW * HW;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
   int64_t j = 0;
   if constexpr (STREAM) j = ctl[1];
