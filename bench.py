@@ -178,7 +178,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (N(0,1) latents, random-init weights)",
-        "config": workload(args, 1), "p50_latency_ms": statistics.median(lat),
+        "config": {**workload(args, 1), "streams_per_gpu": 1, "streams_total": 1, "slots_per_gpu": args.n,
+                   "global_batch": args.n * (2 if args.guidance != 1.0 else 1),
+                   "reference_sample": f"1 stream x {args.n} slots per step on the host CPU; streams are "
+                                       "independent, so frames/s per stream is the per-core-set rate"},
+        "p50_latency_ms": statistics.median(lat),
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -243,8 +247,18 @@ def main():
         return total, steps
 
     clocks = Clocks(local)
+    j0 = sb.j
     total_ms, step_ms = timed(sb.launch, args.steps)
     clk = clocks.stop()
+    # output guard: the last timed step retired generation j-n+1 of every stream, finite
+    want_id = j0 + args.steps - 1 - n + 1
+    fr = sb.frames.float()
+    check = {"frames_finite": bool(torch.isfinite(fr).all().item()),
+             "frame_ids_ok": bool((sb.frame_ids == want_id).all().item()),
+             "frames_abs_mean": float(fr.abs().mean().item()),
+             "ring_finite": bool(torch.isfinite(sb.x_ring).all().item())}
+    if not (check["frames_finite"] and check["frame_ids_ok"] and check["ring_finite"]):
+        raise SystemExit(f"bench output check failed: {check}")
     frames = world * S * args.steps
     value = frames / (total_ms / 1e3)
     lat = [sum(step_ms[i:i + n]) for i in range(max(1, len(step_ms) - n + 1))]
@@ -326,11 +340,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_bench import cpu_stream_throughput
 
-        r = cpu_stream_throughput(model.params, cfg.heads, iters=2, warmup=1, n=n, num_windows=args.windows,
+        iters = 40 if args.model == "s2" else 3
+        r = cpu_stream_throughput(model.params, cfg.heads, iters=iters, warmup=2, n=n, num_windows=args.windows,
                                   w=w, seed=1000)
         cpu = {"value": r["frames_per_s"], "unit": "frames/s", "cores": r["threads"], "kind": "port",
-               "sample": f"1 stream x {n} slots, 2 timed steady-state iterations (+1 warm-up) of the torch-fp32 "
-                         f"{MODELS[args.model][0]} oracle port + numpy Euler step"}
+               "sample": f"1 stream x {n} slots, {iters} timed steady-state iterations (+2 warm-up) of the "
+                         f"torch-fp32 {MODELS[args.model][0]} oracle port + numpy Euler step"}
 
     if rank == 0:
         line = {
@@ -355,6 +370,7 @@ def main():
                                                                / sustained, 4),
                               "flops_per_step": step_flops, "peak_source": f"{src} bf16 sustained"},
             "kernels": per_kernel,
+            "check": check,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,

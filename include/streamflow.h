@@ -77,6 +77,13 @@ typedef struct sf_schedule {
 const char* sf_version(void);
 int sf_device_sm_count(void);
 
+/* Table indices of flow times (schedule.py:201-205 alpha_bar_index and :266-284
+ * grid_indices): abar_idx[i] = clip(floor((1 - t) (t_max - 1) + 0.5)), grid_idx[i] =
+ * nearest inference-grid point (either output may be NULL; grid_idx needs the grid and
+ * status, where SF_STATUS_OFF_GRID / SF_STATUS_TIME_RANGE are OR-ed). */
+int sf_schedule_indices(const sf_schedule* sched, const double* ts, int64_t B, int64_t* abar_idx, int64_t* grid_idx,
+                        uint32_t* status, void* stream);
+
 /* K1 -- window coefficients + grid successor for B flow times.
  * Replaces window_params (schedule.py:224-263), window_lookup (:208-221),
  * alpha_bar_index (:201-205), next_timestep / grid_indices (:266-295).
@@ -263,7 +270,9 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
  * fp32 ring x_ring [S*n, D].  noise_in [S, D] fp32 = initial noise of
  * generation j+1 per stream, or NULL for on-device Philox(noise_seed + s).
  * use_graph != 0 captures the launch sequence into a CUDA graph on first use
- * (keyed by the buffer pointers) and replays it afterwards. */
+ * and replays it afterwards; the cache key is every argument the capture bakes
+ * in (all pointers, S, n, m, w, noise_seed), so a replay always equals the
+ * eager launch sequence for the same arguments. */
 int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
                        const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
@@ -281,6 +290,12 @@ int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m
 
 /* Number of kernel launches this handle has issued or captured so far. */
 int64_t sf_dit_launch_count(const sf_dit* h);
+
+/* Destroy every cached stream-step graph whose ring control word is ctl (the
+ * owner of those buffers calls this before freeing them); synchronises the device
+ * if any graph is released.  sf_dit_graph_count: graphs currently cached. */
+int sf_dit_graph_release(sf_dit* h, const int64_t* ctl);
+int64_t sf_dit_graph_count(const sf_dit* h);
 
 /* Reset a fp32 ring: generation-0 noise into slot 0 of each stream (noise0 [S, D]
  * or Philox when NULL), ctl <- j = 0. */

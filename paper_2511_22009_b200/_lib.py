@@ -40,6 +40,7 @@ SIGNATURES = {
     "sf_version": [],
     "sf_device_sm_count": [],
     "sf_window_params": [C.POINTER(SfSchedule), _vp, _i64, _vp, _vp, _vp],
+    "sf_schedule_indices": [C.POINTER(SfSchedule), _vp, _i64, _vp, _vp, _vp, _vp],
     "sf_velocity_step": [_vp, C.c_int, _vp, _vp, C.c_int, _vp, _i64, _i64, _vp],
     "sf_cfg_combine": [_vp, C.c_int, _i64, _i64, _f64, _vp, _vp],
     "sf_mock_keys": [_i64, _vp, _vp, _vp, _i64, _i32, _vp, _vp],

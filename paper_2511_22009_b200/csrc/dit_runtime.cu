@@ -811,9 +811,13 @@ struct sf_dit {
   GemmMaps g_ada;                                  // TMA descriptors per GEMM call site
   std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
   AttnMaps attn_maps;
-  std::map<std::tuple<const void*, int64_t, int, int64_t, double, const void*, const void*, const void*>,
-           cudaGraphExec_t>
-      graphs;
+  // One instantiated graph per distinct argument set of sf_dit_stream_step: every pointer and
+  // value the capture bakes into a launch is part of the key, so a replay is always the launch
+  // sequence an eager call with the same arguments would enqueue.  Owners release their graphs
+  // (sf_dit_graph_release) when their buffers are freed; the cache is also capped.
+  using GraphKey = std::tuple<const void*, int64_t, int, int64_t, const void*, const void*, const void*, const void*,
+                              const void*, const void*, double, const void*, uint64_t, const void*, const void*>;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
   // profiling / accounting
   int64_t launch_count = 0;
@@ -821,6 +825,8 @@ struct sf_dit {
   std::vector<cudaEvent_t> prof_events;
   std::vector<int> prof_cls;
 };
+
+static constexpr size_t kMaxGraphs = 16;
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -1274,10 +1280,16 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
   if (!use_graph)
     return stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
                                 noise_seed, frames_out, frame_ids, st);
-  auto key = std::make_tuple((const void*)x_ring, S, n, m, w, (const void*)noise_in, (const void*)frames_out,
-                             (const void*)ctl);
+  const sf_dit::GraphKey key{(const void*)ctl, S,          n, m, (const void*)stage_params, (const void*)row_info,
+                             (const void*)row_t, (const void*)x_ring, (const void*)emb, (const void*)neg, w,
+                             (const void*)noise_in, noise_seed, (const void*)frames_out, (const void*)frame_ids};
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
+    if (h->graphs.size() >= kMaxGraphs) {  // cap: drop every cached graph (re-captured on next use)
+      cudaStreamSynchronize(st);
+      for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+      h->graphs.clear();
+    }
     // Capture on a private stream (the caller's may be the legacy default
     // stream, which cannot be captured); the graph is launched on the caller's.
     if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
@@ -1296,6 +1308,24 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
   }
   return cudaGraphLaunch(it->second, st) == cudaSuccess ? SF_OK : SF_ERR_CUDA;
 }
+
+int sf_dit_graph_release(sf_dit* h, const int64_t* ctl) {
+  if (!h) return SF_ERR_PARAMETER;
+  bool any = false;
+  for (auto it = h->graphs.begin(); it != h->graphs.end();) {
+    if (std::get<0>(it->first) == (const void*)ctl) {
+      if (!any) cudaDeviceSynchronize();  // a replay of this graph may still be in flight
+      any = true;
+      cudaGraphExecDestroy(it->second);
+      it = h->graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  return SF_OK;
+}
+
+int64_t sf_dit_graph_count(const sf_dit* h) { return h ? (int64_t)h->graphs.size() : -1; }
 
 int sf_dit_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, float* x_ring, const float* noise0,
                         uint64_t noise_seed, void* stream) {

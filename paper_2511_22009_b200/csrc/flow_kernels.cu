@@ -20,6 +20,16 @@ __device__ __forceinline__ int abar_index(double tau, int t_max) {
   return idx < 0 ? 0 : (idx > t_max - 1 ? t_max - 1 : idx);
 }
 
+// grid_indices (schedule.py:266-284): nearest of grid[pos-1], grid[pos] (ties to the upper)
+__device__ __forceinline__ int grid_index(const sf_schedule& s, double t) {
+  const int G = s.num_steps;
+  int pos = 0;
+  while (pos < G && s.grid[pos] < t) ++pos;  // searchsorted(side='left')
+  const int lo = pos - 1 < 0 ? 0 : (pos - 1 > G - 1 ? G - 1 : pos - 1);
+  const int hi = pos > G - 1 ? G - 1 : pos;
+  return fabs(__dsub_rn(s.grid[hi], t)) <= fabs(__dsub_rn(s.grid[lo], t)) ? hi : lo;
+}
+
 __device__ void window_coeffs_row(const sf_schedule& s, double t, double* p, uint32_t& status) {
   if (!(t >= 0.0 && t <= 1.0)) status |= SF_STATUS_TIME_RANGE;
   // window_lookup (schedule.py:208-221): count interior boundaries strictly below t (+eps)
@@ -39,11 +49,7 @@ __device__ void window_coeffs_row(const sf_schedule& s, double t, double* p, uin
   const double eta_t = __ddiv_rn(__dmul_rn(eta_s, __dsub_rn(t_e, t)), denom);
   // grid_indices / next_timestep (schedule.py:266-295)
   const int G = s.num_steps;
-  int pos = 0;
-  while (pos < G && s.grid[pos] < t) ++pos;  // searchsorted(side='left')
-  const int lo = pos - 1 < 0 ? 0 : (pos - 1 > G - 1 ? G - 1 : pos - 1);
-  const int hi = pos > G - 1 ? G - 1 : pos;
-  const int idx = fabs(__dsub_rn(s.grid[hi], t)) <= fabs(__dsub_rn(s.grid[lo], t)) ? hi : lo;
+  const int idx = grid_index(s, t);
   double t_next;
   if (fabs(__dsub_rn(s.grid[idx], t)) > s.eps) {
     status |= SF_STATUS_OFF_GRID;
@@ -73,6 +79,21 @@ __global__ void window_params_kernel(sf_schedule s, const double* __restrict__ t
   uint32_t st = 0;
   window_coeffs_row(s, ts[i], out + i * SF_PARAM_STRIDE, st);
   if (st) atomicOr(status, st);
+}
+
+__global__ void schedule_indices_kernel(sf_schedule s, const double* __restrict__ ts, int64_t B, int64_t* abar_idx,
+                                        int64_t* grid_idx, uint32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const double t = ts[i];
+  if (abar_idx) abar_idx[i] = abar_index(t, s.t_max);
+  if (grid_idx) {
+    uint32_t st = (t >= 0.0 && t <= 1.0) ? 0u : (uint32_t)SF_STATUS_TIME_RANGE;
+    const int g = grid_index(s, t);
+    if (fabs(__dsub_rn(s.grid[g], t)) > s.eps) st |= SF_STATUS_OFF_GRID;
+    grid_idx[i] = g;
+    if (st) atomicOr(status, st);
+  }
 }
 
 // ============================================================ K10-lite: Euler step
@@ -354,6 +375,15 @@ __global__ void analytic_eps_kernel(const double* __restrict__ A, const double* 
 }  // namespace sf
 
 extern "C" {
+
+int sf_schedule_indices(const sf_schedule* sched, const double* ts, int64_t B, int64_t* abar_idx, int64_t* grid_idx,
+                        uint32_t* status, void* stream) {
+  if (!sched || !ts || B < 1 || sched->t_max < 1 || (grid_idx && (!status || sched->num_steps < 1 || !sched->grid)))
+    return SF_ERR_PARAMETER;
+  schedule_indices_kernel<<<(unsigned)((B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*sched, ts, B, abar_idx,
+                                                                                         grid_idx, status);
+  return cuda_status();
+}
 
 int sf_window_params(const sf_schedule* sched, const double* ts, int64_t B, double* out, uint32_t* status,
                      void* stream) {

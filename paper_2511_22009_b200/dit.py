@@ -148,8 +148,11 @@ _lib.SIGNATURES.update({
                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                             C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "sf_dit_launch_count": [C.c_void_p],
+    "sf_dit_graph_release": [C.c_void_p, C.c_void_p],
+    "sf_dit_graph_count": [C.c_void_p],
 })
 _lib.RESTYPES["sf_dit_launch_count"] = C.c_int64
+_lib.RESTYPES["sf_dit_graph_count"] = C.c_int64
 
 PROFILE_CLASSES = ("prepare", "cond", "adaln_gemm", "patch_embed_ln", "qkv_gemm", "attention",
                    "proj_gemm_res_ln", "fc1_gemm_gelu", "fc2_gemm_res_ln", "final_euler_refill", "mlp_fused", "block_tail")

@@ -213,6 +213,10 @@ class StreamBatch:
         self.noise_dev = torch.zeros(self.S, self.D, dtype=noise_dt, device=dev)
         self.noise_host = torch.zeros(self.S, self.D, dtype=noise_dt).pin_memory() if noise == "numpy_host" else None
         self.noise_seed = int(self.seeds[0]) & ((1 << 64) - 1)
+        if noise in ("device", "host") and any(int(v) != int(self.seeds[0]) + s for s, v in enumerate(self.seeds)):
+            # the Philox generator of stream s is keyed by seeds[0] + s
+            raise ParameterError("noise='device'/'host' keys stream s's Philox noise by seeds[0] + s; "
+                                 "pass consecutive seeds (or noise='numpy' for arbitrary per-stream seeds)")
         if noise == "numpy":
             if any(int(v) < 0 for v in self.seeds):
                 raise ValueError("expected non-negative integer")  # numpy's SeedSequence error
@@ -230,6 +234,14 @@ class StreamBatch:
         self.j = 0
         self._stream = lambda: torch.cuda.current_stream().cuda_stream
         self.reset()
+
+    def __del__(self):
+        # drop the CUDA graphs captured over this batch's buffers before they are freed
+        if getattr(self, "kind", None) == "dit" and getattr(self, "use_graph", False):
+            try:
+                _lib.fn("sf_dit_graph_release")(self.model.device_model.handle, self.ctl.data_ptr())
+            except Exception:
+                pass
 
     # ------------------------------------------------------------------ admission noise
     def _fill_noise(self, gen: int) -> bool:
@@ -278,6 +290,10 @@ class StreamBatch:
         if self.done():
             raise StateError("stream batch already drained all generations")
         j, n, m, st = self.j, self.n, self.m, self._stream()
+        if self.kind != "generic":
+            # the fused step is the iteration's one guided forward: charge the model's declared
+            # cost once, as VelocityModel.forward does (models.py:111-114)
+            busy_wait_us(self.model.cost_us)
         admit_next = self._fill_noise(j + 1) if self.noise in ("numpy", "numpy_host") else (j + 1 < m)
         if self.kind == "dit":
             _lib.call("sf_dit_stream_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, n, m,

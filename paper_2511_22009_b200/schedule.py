@@ -205,6 +205,34 @@ def window_params(ts, sched: TimeWindowSchedule) -> WindowParams:
                         lambda_t=o[:, _lib.P_LAMBDA_T], eta_t=o[:, _lib.P_ETA_T])
 
 
+def alpha_bar_index(ts, t_max: int) -> np.ndarray:
+    """Noise-table index per flow time, round half up, clamped (schedule.py:201-205), on
+    the GPU with the same fp64 operation order the window kernel uses."""
+    t = _device_ts(ts)
+    out = torch.empty(t.numel(), dtype=torch.int64, device=t.device)
+    s = _lib.SfSchedule(None, None, None, 0, int(t_max), 0, 0, 0.0)
+    _lib.call("sf_schedule_indices", C.byref(s), t.data_ptr(), t.numel(), out.data_ptr(), None, None,
+              torch.cuda.current_stream().cuda_stream)
+    return out.cpu().numpy()
+
+
+def grid_indices(ts, sched: TimeWindowSchedule) -> np.ndarray:
+    """Inference-grid index per t within eps (schedule.py:266-284); TimeDomainError when
+    a t is out of [0, 1] or off the grid."""
+    dev = DeviceSchedule.of(sched)
+    t = _device_ts(ts)
+    out = torch.empty(t.numel(), dtype=torch.int64, device=t.device)
+    dev.status.zero_()
+    _lib.call("sf_schedule_indices", C.byref(dev.struct), t.data_ptr(), t.numel(), None, out.data_ptr(),
+              dev.status.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    st = int(dev.status.item())
+    if st & _lib.SF_STATUS_TIME_RANGE:
+        raise TimeDomainError(f"timesteps outside [0, 1]: {np.asarray(ts).reshape(-1)[:4]}")
+    if st & _lib.SF_STATUS_OFF_GRID:
+        raise TimeDomainError("timesteps not on the inference grid")
+    return out.cpu().numpy()
+
+
 def window_lookup(ts, sched: TimeWindowSchedule) -> np.ndarray:
     """Window index per t (schedule.py:208-221), derived from the device t_s."""
     wp = window_params(ts, sched)

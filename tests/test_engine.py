@@ -107,3 +107,24 @@ def test_run_stream_through_compiled_engine_matches_plain_model():
     for a, b in zip(er, pr):
         assert a.id == b.id and np.array_equal(a.latent, b.latent)
     assert engine.stats.calls_decomposed > 0 and engine.stats.calls_homogeneous > 0
+
+
+@pytest.mark.gpu
+def test_dit_engine_graph_replay_bit_exact():
+    """The CUDA-graph engine over the DiT: homogeneous batches replay one graph per batch size,
+    mixed batches replay the rows=1 graph per row; both bit-identical to inner._compute."""
+    from paper_2511_22009_b200.dit import DIT_S2
+
+    model = sf.DiTVelocityModel(DIT_S2, seed=12, max_rows=4, bias_std=0.02)
+    engine = sf.CompiledEngine(model)
+    rng = np.random.default_rng(5)
+    cond = sf.make_conditioning(rng.standard_normal(8))
+    for ts in ([0.5] * 4, [0.25, 0.75, 0.0], [0.5] * 6, [0.25] * 4, [0.0, 0.5]):
+        x = rng.standard_normal((len(ts), model.dim)).astype(np.float32)
+        batch = sf.make_latent_batch(x, np.asarray(ts), np.arange(len(ts)))
+        out = sf.adaptive_forward(engine, batch, cond)
+        assert np.array_equal(out.epsilon, model._compute(batch, cond).epsilon), ts
+    gs = engine.graph_stats
+    assert sorted(gs.sizes) == [1, 4, 6]  # one capture per batch size (6 rows = two launch sequences)
+    assert gs.replays == engine.invocations == 1 + 3 + 1 + 1 + 2 and gs.eager_calls == 0
+    assert engine.stats.calls_homogeneous == 3 and engine.stats.calls_decomposed == 2

@@ -72,3 +72,87 @@ def test_graph_replay_equals_eager(setup):
     for a, b in zip(outs[0], outs[1]):
         for ra, rb in zip(a, b):
             assert ra.id == rb.id and np.array_equal(ra.latent, rb.latent)
+
+
+def _oracle_eps_gpu(params_gpu, emb, neg, w, heads):
+    """Guided eps of the fp32 DiT reference run on the GPU (TF32 off), in the reference's
+    CFG layout: [uncond (neg or zeros) ; cond] combined as e_u + w (e_c - e_u)
+    (models.py:257-268, :288-293)."""
+    def eps_fn(ids, ts, x):
+        B = len(ids)
+        xt = torch.from_numpy(np.asarray(x, np.float32)).view(B, 4, 64, 64).cuda()
+        tt = torch.as_tensor(ts, dtype=torch.float64).cuda()
+        ec = torch.as_tensor(np.tile(emb, (B, 1))).cuda()
+        e_c = dit_forward(params_gpu, xt, tt, ec, heads=heads).reshape(B, -1)
+        if w == 1.0:
+            return e_c.cpu().numpy()
+        en = torch.zeros_like(ec) if neg is None else torch.as_tensor(np.tile(neg, (B, 1))).cuda()
+        e_u = dit_forward(params_gpu, xt, tt, en, heads=heads).reshape(B, -1)
+        return (e_u + w * (e_c - e_u)).cpu().numpy()
+    return eps_fn
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_dit_cfg_negative_embedding_short_grids(setup, n):
+    """configs[2]: CFG (w=7.5) with a NON-ZERO negative embedding on 1- and 2-step grids,
+    through the fused stream step (the fused kernel's neg pointer), vs the oracle loop."""
+    from oracle.dit_oracle import params_to
+
+    sf, model = setup
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    S, m, w, D = 2, 3, 7.5, model.dim
+    sched = sf.build_time_window_schedule(num_windows=4, inference_steps=n)
+    rng = np.random.default_rng(20 + n)
+    embs = [rng.standard_normal(8) for _ in range(S)]
+    negs = [rng.standard_normal(8) for _ in range(S)]
+    conds = [sf.make_conditioning(embs[s], guidance_scale=w, negative_embedding=negs[s]) for s in range(S)]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=70, m=m, dtype=np.float32)
+    out = sb()
+    osch = O.make_schedule(num_windows=4, steps=n)
+    pg = params_to(model.params, "cuda")
+    tol = TRAJ_TOL * max(1.0, (2 * w - 1) / 3)
+    for s in range(S):
+        run = O.run_stream(m, n, _oracle_eps_gpu(pg, embs[s], negs[s], w, 6), 70 + s, osch, D, dtype=np.float32)
+        assert [r.id for r in out[s]] == run.order
+        for r in out[s]:
+            want = run.latents[r.id]
+            err = np.abs(r.latent - want).max() / np.abs(want).max()
+            print(f"n={n} stream {s} gen {r.id}: normalised max err {err:.2e} (tol {tol:.1e})")
+            assert err <= tol, (s, r.id, err)
+        assert sb.stats[s].model_calls == m + n - 1
+    # the negative embedding matters: the zero-negative run differs
+    conds0 = [sf.make_conditioning(embs[s], guidance_scale=w) for s in range(S)]
+    out0 = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds0, seed=70, m=m, dtype=np.float32)()
+    assert not np.array_equal(out0[0][0].latent, out[0][0].latent)
+
+
+def test_dit_xl_stream_step_matches_oracle():
+    """configs[3]: the DiT-XL/2 fused stream step (final layer <1152> in stream mode,
+    hd-72 attention, RES + LayerNorm pass) over an 8-slot batch (S=2 x n=4) vs the oracle
+    loop driving the fp32 XL reference on the GPU.  Tolerance: the XL forward bound (3e-2,
+    tests/test_gpu_dit_xl.py) carried through the trajectory."""
+    import paper_2511_22009_b200 as sf
+    from oracle.dit_oracle import params_to
+    from paper_2511_22009_b200.dit import DIT_XL2
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    model = sf.DiTVelocityModel(DIT_XL2, seed=4, max_rows=8, bias_std=0.02)
+    S, m, n, D = 2, 2, 4, model.dim
+    sched = sf.build_time_window_schedule(num_windows=3, inference_steps=n)
+    rng = np.random.default_rng(8)
+    embs = [rng.standard_normal(8) for _ in range(S)]
+    conds = [sf.make_conditioning(embs[s]) for s in range(S)]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=90, m=m, dtype=np.float32)
+    out = sb()
+    osch = O.make_schedule(num_windows=3, steps=n)
+    pg = params_to(model.params, "cuda")
+    for s in range(S):
+        run = O.run_stream(m, n, _oracle_eps_gpu(pg, embs[s], None, 1.0, 16), 90 + s, osch, D, dtype=np.float32)
+        assert [r.id for r in out[s]] == run.order
+        for r in out[s]:
+            want = run.latents[r.id]
+            err = np.abs(r.latent - want).max() / np.abs(want).max()
+            print(f"XL stream {s} gen {r.id}: normalised max err {err:.2e}")
+            assert err <= 3 * TRAJ_TOL, (s, r.id, err)
