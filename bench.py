@@ -48,8 +48,11 @@ def parse():
     ap.add_argument("--n", type=int, default=4, help="steps per generation (slots per stream)")
     ap.add_argument("--windows", type=int, default=4, help="time windows K of the scheduler")
     ap.add_argument("--guidance", type=float, default=1.0)
-    ap.add_argument("--model", default="s2", choices=["s2", "xl2"],
-                    help="s2: DiT-S/2 (configs[1]); xl2: DiT-XL/2 (configs[3], 8-slot batch = 2 streams x 4)")
+    ap.add_argument("--model", default="s2", choices=["s2", "xl2", "mock"],
+                    help="s2: DiT-S/2 (configs[1]); xl2: DiT-XL/2 (configs[3], 8-slot batch = 2 streams x 4); "
+                         "mock: the reference's SeededMockModel at D=16384 (configs[0]), beside the reference "
+                         "package's own run_stream on the host")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"], help="latent dtype of --model mock")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the separately timed TAESD decode line")
     return ap.parse_args()
@@ -61,9 +64,179 @@ def env_rank():
 
 
 MODELS = {
+    "mock": ("SeededMockModel", "reference SeededMockModel (blake2b row key + splitmix64), D=16384, no network"),
     "s2": ("DiT-S/2", "DiT-S/2 (depth 12, hidden 384, 6 heads, patch 2, 1024 tokens)"),
     "xl2": ("DiT-XL/2", "DiT-XL/2 (depth 28, hidden 1152, 16 heads of 72, patch 2, 1024 tokens)"),
 }
+
+
+def run_reference_mock(args):
+    """--impl reference --model mock: the reference package's own flowpipe.run_stream +
+    SeededMockModel on every host core (one stream per process), bounded sample."""
+    rank, _, _ = env_rank()
+    if rank != 0:
+        return 0
+    from oracle.ref_mock_bench import time_reference_mock
+
+    procs = os.cpu_count() or 1
+    m = 150
+    for _ in range(max(1, args.warmup // 3)):
+        time_reference_mock(m=8, n=args.n, dtype=args.dtype, procs=1)
+    runs = [time_reference_mock(m=m, n=args.n, dtype=args.dtype, procs=procs) for _ in range(max(1, args.steps // 10))]
+    r = max(runs, key=lambda x: x["frames_per_s"])
+    one = time_reference_mock(m=m, n=args.n, dtype=args.dtype, procs=1)
+    value = r["frames_per_s"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (numpy generation noise, hash mock model)",
+        "config": {**mock_workload(args, 1), "streams_per_gpu": procs, "streams_total": procs,
+                   "reference_sample": r["sample"]},
+        "p50_latency_ms": one["p50_latency_ms"], "single_stream_frames_per_s": one["frames_per_s"],
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": r["kind"], "sample": r["sample"]},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def mock_workload(args, world):
+    return {
+        "workload": f"reference SeededMockModel velocity field (D=16384 = 64x64x4 latent), {args.n}-step heterogeneous "
+                    f"stream batch, {args.streams} streams/GPU x {args.n} slots, {args.dtype} latents, numpy-identical "
+                    "admission noise (BASELINE configs[0] workload on the device path)",
+        "model": MODELS["mock"][1], "streams_per_gpu": args.streams, "streams_total": args.streams * world,
+        "slots_per_gpu": args.streams * args.n, "steps_per_generation": args.n, "time_windows": args.windows,
+        "guidance_scale": args.guidance, "global_batch": args.streams * args.n * world, "seq_len": 16384,
+        "parallelism": f"stream-partitioned x{world} (no collective in the step)",
+        "l2": "ring + noise + frames per step > 126 MB L2 at S >= 256 (no flush needed)",
+    }
+
+
+def run_mock(args):
+    """Our arm for --model mock: the fused device stream step (sf_stream_mock_step: guided hash
+    eps + Euler + emit + refill) with on-device numpy-identical noise (sf_numpy_normal)."""
+    rank, world, local = env_rank()
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_22009_b200.build import build
+
+    build()
+    import paper_2511_22009_b200 as sf
+    from paper_2511_22009_b200.partition import stream_partition, stream_seeds
+
+    S, n, D = args.streams, args.n, 16384
+    dt = np.float64 if args.dtype == "f64" else np.float32
+    esz = 8 if args.dtype == "f64" else 4
+    model = sf.SeededMockModel(dim=D, seed=0)
+    sched = sf.build_time_window_schedule(num_windows=args.windows, inference_steps=n)
+    mine = stream_partition(S * world, world, rank)
+    seeds = stream_seeds(1000, mine)
+    conds = [sf.make_conditioning(np.random.default_rng([sd, 2**32 - 1]).standard_normal(8), guidance_scale=args.guidance)
+             for sd in seeds]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, dtype=dt, noise="numpy")
+    for _ in range(args.warmup):
+        sb.launch()
+    torch.cuda.synchronize()
+
+    def timed(fn, K):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(K):
+            fn()
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total = ev[0].elapsed_time(ev[K])
+        if world > 1:
+            t = torch.tensor([total], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return total, [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
+
+    clocks = Clocks(local)
+    total_ms, step_ms = timed(sb.launch, args.steps)
+    clk = clocks.stop()
+    frames = world * S * args.steps
+    value = frames / (total_ms / 1e3)
+    lat = [sum(step_ms[i:i + n]) for i in range(max(1, len(step_ms) - n + 1))]
+    fr = sb.frames.float()
+    check = {"frames_finite": bool(torch.isfinite(fr).all().item()),
+             "frame_ids_ok": bool((sb.frame_ids == sb.j - n).all().item())}
+    if not all(check.values()):
+        raise SystemExit(f"bench output check failed: {check}")
+    # per-kernel split of one step (events between the three launches of StreamBatch.launch)
+    st = torch.cuda.current_stream().cuda_stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record()
+    sf.numpy_noise_device(sb.seeds_dev, sb.j + 1, D, out=sb.noise_dev)
+    ev[1].record()
+    sf._lib.call("sf_stream_prepare", sb.ctl.data_ptr(), S, n, sb.m, sb.stage_params.data_ptr(),
+                 sb.row_info.data_ptr(), sb.row_t.data_ptr(), st)
+    ev[2].record()
+    sf._lib.call("sf_stream_mock_step", sb.ctl.data_ptr(), S, n, sb.m, D,
+                 sf._lib.SF_F64 if dt == np.float64 else sf._lib.SF_F32, sb.x_ring.data_ptr(),
+                 sb.stage_params.data_ptr(), sb.row_info.data_ptr(), sb.row_t.data_ptr(), model.seed,
+                 sb.emb.data_ptr(), None, 8, sb.w, sb.noise_dev.data_ptr(), sb.frames.data_ptr(),
+                 sb.frame_ids.data_ptr(), st)
+    ev[3].record()
+    torch.cuda.synchronize()
+    sb.j += 1
+    noise_ms, step_k_ms = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+    # algorithmic bytes of sf_stream_mock_step: ring read + write (S n D), noise read + frames write (S D)
+    step_bytes = S * n * D * esz * 2 + S * D * (8 + esz)
+    _, _, hbm, src = peaks()
+
+    # e2e through the public API with host buffers: H2D admission noise, D2H frames
+    sb_e2e = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, dtype=dt, noise="host")
+    pool = [torch.randn(S, D, dtype=torch.float64).pin_memory() for _ in range(2)]
+    fdst = torch.empty(S, D, dtype=sb_e2e.frames.dtype).pin_memory()
+    it = {"i": 0}
+
+    def e2e_step():
+        it["i"] += 1
+        sb_e2e.launch_host_io(pool[it["i"] % 2], fdst)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    e2e_ms, _ = timed(e2e_step, args.steps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.ref_mock_bench import time_reference_mock
+
+        r = time_reference_mock(m=150, n=n, dtype=args.dtype, procs=os.cpu_count() or 1)
+        cpu = {"value": r["frames_per_s"], "unit": "frames/s", "cores": r["procs"], "kind": r["kind"],
+               "sample": r["sample"]}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (numpy-identical generation noise drawn on the device, reference hash mock model)",
+            "config": mock_workload(args, world), "p50_latency_ms": statistics.median(lat),
+            "p99_latency_ms": float(np.percentile(lat, 99)),
+            "e2e": {"value": frames / (e2e_ms / 1e3), "unit": "frames/s", "h2d_bytes_per_step": S * D * 8,
+                    "d2h_bytes_per_step": S * D * esz},
+            "roofline": {"bound": "hbm", "kernel": "stream_mock_step", "achieved": round(step_bytes / step_k_ms / 1e6, 1),
+                         "peak": hbm, "unit": "GB/s", "frac": round(step_bytes / step_k_ms / 1e6 / hbm, 4),
+                         "traffic": None, "peak_source": f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+                         "bytes_per_launch": step_bytes, "kernel_ms": round(step_k_ms, 4)},
+            "kernels": {"numpy_normal (admission noise)": round(noise_ms, 4), "stream_mock_step": round(step_k_ms, 4)},
+            "check": check, "cpu_baseline": cpu, "gpu_launches": 3 * args.steps, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 def model_cfg(args):
@@ -195,8 +368,15 @@ def main():
     args = parse()
     if args.model == "xl2" and "--streams" not in sys.argv:
         args.streams = 2  # configs[3]: 8-slot stream batch (2 streams x 4 slots) per GPU
+    if args.model == "mock" and "--streams" not in sys.argv:
+        args.streams = 256
+    if args.model == "mock" and "--steps" not in sys.argv:
+        args.steps = 400  # ~0.5 ms per step: a timed region long enough for the clock sampler
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference_mock(args) if args.model == "mock" else run_reference(args)
+    if args.model == "mock":
+        args.warmup = max(args.warmup, 3, args.n)
+        return run_mock(args)
     args.warmup = max(args.warmup, 3, args.n)
     rank, world, local = env_rank()
     import torch
@@ -215,7 +395,7 @@ def main():
     rows = S * n * (2 if w != 1.0 else 1)
     model = sf.DiTVelocityModel(cfg, seed=0, max_rows=rows)
     sched = sf.build_time_window_schedule(num_windows=args.windows, inference_steps=n)
-    from paper_2511_22009_b200.partition import gather_frames, reduce_counts, stream_partition, stream_seeds
+    from paper_2511_22009_b200.partition import reduce_counts, stream_partition, stream_seeds
 
     mine = stream_partition(S * world, world, rank)  # weak scaling: S streams per GPU
     seeds = stream_seeds(1000, mine)
@@ -331,10 +511,17 @@ def main():
     # ---- stream-partitioned output: NCCL gather of the last frames + frame counts (off the timed region)
     gathered = None
     if world > 1:
-        allf, ids = gather_frames(sb.frames, sb.frame_ids)
+        # one window of n steps after the timed region: every frame each rank emits, gathered once
+        from paper_2511_22009_b200.partition import FrameWindow
+
+        fw = FrameWindow(sb, window=n)
+        for _ in range(n):
+            sb.launch()
+            fw.record()
+        allf, ids = fw.gather()
         cnt = reduce_counts([S * args.steps, sb.stats[0].model_calls], "cuda")
-        gathered = {"frames_gathered": int(allf.shape[0]), "frame_ids_valid": int((ids >= 0).sum().item()),
-                    "frames_emitted_timed_total": cnt[0]}
+        gathered = {"window_steps": n, "frames_gathered": int(allf.shape[0] * allf.shape[1]),
+                    "frame_ids_valid": int((ids >= 0).sum().item()), "frames_emitted_timed_total": cnt[0]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -60,6 +60,7 @@ SIGNATURES = {
     "sf_attention": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
     "sf_attention_hd": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp],
     "sf_numpy_normal": [_vp, _i64, _i64, _i64, _vp, C.c_int, _vp],
+    "sf_philox_normal": [_vp, _i64, _i64, C.c_uint64, _i64, _vp],
     "sf_mlp_fused": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, _i64, _i32, _vp],
     "sf_block_tail": [_vp] * 15 + [_i64, C.c_float, _i64, _i32, _vp],
 }
@@ -93,7 +94,9 @@ def load():
 def fn(name: str):
     """The library function ``name`` with its ctypes signature applied."""
     f = getattr(load(), name)
-    if name in SIGNATURES and f.argtypes is None:
+    if name not in SIGNATURES:  # ctypes would pass 64-bit pointers / seeds as 32-bit ints
+        raise RuntimeError(f"{name}: no ctypes signature registered")
+    if f.argtypes is None:
         f.argtypes = SIGNATURES[name]
         f.restype = RESTYPES.get(name, C.c_int)
     return f

@@ -143,7 +143,6 @@ _lib.SIGNATURES.update({
                            C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
     "sf_dit_stream_reset": [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                             C.c_uint64, C.c_void_p],
-    "sf_philox_normal": [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p],
     "sf_dit_profile_step": [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                             C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],

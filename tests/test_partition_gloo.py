@@ -66,3 +66,47 @@ def test_gather_frames_world2(total):
     for g, row in enumerate(frames):
         assert row == [float(g)] * D
     assert counts == [total, 30]
+
+
+def _window_worker(rank, world, port, total, D, steps, q):
+    """CPU stand-in for a StreamBatch: frame of (stream g, step k) = g * 100 + k."""
+    from paper_2511_22009_b200.partition import FrameWindow
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = stream_partition(total, world, rank)
+
+    class FakeBatch:
+        frames = torch.zeros(len(mine), D)
+        frame_ids = torch.zeros(len(mine), dtype=torch.int64)
+
+    fw = FrameWindow(FakeBatch, window=steps)
+    for k in range(steps):
+        FakeBatch.frames.copy_(torch.tensor([[g * 100.0 + k] * D for g in mine]))
+        FakeBatch.frame_ids.fill_(k - 1)
+        fw.record()
+    f, ids = fw.gather()
+    if rank == 0:
+        q.put((f.numpy().tolist(), ids.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_frame_window_gathers_every_step_world2():
+    """FrameWindow: every step's frames of every rank, in (step, global stream) order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    total, D, steps = 5, 3, 4
+    procs = [ctx.Process(target=_window_worker, args=(r, 2, port, total, D, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    frames, ids = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(frames) == steps and all(len(f) == total for f in frames)
+    for k in range(steps):
+        assert ids[k] == [k - 1] * total
+        for g in range(total):
+            assert frames[k][g] == [g * 100.0 + k] * D
