@@ -668,6 +668,14 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
                       float q_scale) {
   using namespace tail;
   if (M % BM || T % BM) return SF_ERR_PARAMETER;
+  static int pair = -1;  // TEMP A/B switch (SF_TAIL_PAIR=0: single-CTA kernel)
+  if (pair < 0) {
+    const char* e = getenv("SF_TAIL_PAIR");
+    pair = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (pair && !wqkv && M % (2 * BM) == 0)
+    return launch_block_tail_pair(attn, wproj, bproj, w1, w2, b1, b2, xres, xmod_out, gate1, shift1, scale1, gate2,
+                                  shift2, scale2, vec_stride, ln_eps, M, T, st);
   static bool attr = false;
   if (!attr) {
     const cudaError_t err = cudaFuncSetAttribute(block_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);

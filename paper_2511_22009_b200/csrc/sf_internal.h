@@ -51,6 +51,12 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
                       cudaStream_t st, const void* wqkv = nullptr, const float* bqkv = nullptr, void* q = nullptr,
                       void* k = nullptr, void* vt = nullptr, int heads = 0, float q_scale = 0.f);
 
+int launch_block_tail_pair(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
+                           const float* b1, const float* b2, __nv_bfloat16* xres, __nv_bfloat16* xmod_out,
+                           const float* gate1, const float* shift1, const float* scale1, const float* gate2,
+                           const float* shift2, const float* scale2, int64_t vec_stride, float ln_eps, int64_t M, int T,
+                           cudaStream_t st);
+
 inline int cuda_status() { return cudaGetLastError() == cudaSuccess ? SF_OK : SF_ERR_CUDA; }
 
 // Programmatic dependent launch (PDL) for the per-layer chain QKV GEMM -> attention ->
