@@ -488,7 +488,7 @@ def main():
         "qkv_gemm": L * 2.0 * M * 3 * H * H, "attention": L * 4.0 * rows * T * T * H,
         "proj_gemm_res_ln": L * 2.0 * M * H * H, "fc1_gemm_gelu": L * 2.0 * M * Fm * H,
         "fc2_gemm_res_ln": L * 2.0 * M * H * Fm, "adaln_gemm": 2.0 * rows * (6 * H * L + 2 * H) * H,
-        "mlp_fused": L * 4.0 * M * H * Fm, "block_tail": L * (4.0 * M * H * Fm + 2.0 * M * H * H),
+        "block_tail": L * (4.0 * M * H * Fm + 2.0 * M * H * H),
     }
     burst, sustained, hbm, src = peaks()
     dom = max(flops, key=lambda k: prof[k][0])

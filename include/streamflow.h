@@ -181,28 +181,16 @@ int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float
 int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, void* xmod, const float* gate,
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream);
-/* Fused DiT-S/2 MLP block (hidden 384, MLP 1536): xres += gate * (GELU(xmod W1^T + b1) W2^T + b2);
- * xmod = LN(xres) * (1 + scale) + shift -- the hidden never leaves the SM.  xmod is read
- * (this block's modulated input) and overwritten (the next LayerNorm's output).
- * M and tokens_per_slot multiples of 128. */
-int sf_mlp_fused(const void* xmod_in, const void* w1, const void* w2, const float* b1, const float* b2, void* xres,
-                 void* xmod_out, const float* gate, const float* shift, const float* scale, int64_t vec_stride,
-                 float ln_eps, int64_t M, int32_t tokens_per_slot, void* stream);
-/* Post-attention half of a DiT-S/2 block in one kernel: attention projection + gated residual
- * + LayerNorm/modulate (kept on chip) + the fused MLP + gated residual + next LayerNorm/modulate.
- * attn [M, 384] bf16; wproj [384, 384]; xres updated in place; xmod_out = next LN output. */
+/* Post-attention half of a DiT-S/2 block in one kernel on CTA pairs: attention projection +
+ * gated residual + LayerNorm/modulate (kept on chip) + MLP (fc1 + GELU + fc2, the hidden kept on
+ * chip) + gated residual + next LayerNorm/modulate.  attn [M, 384] bf16; wproj [384, 384];
+ * w1 [1536, 384]; w2 [384, 1536]; xres updated in place; xmod_out = next LN output.
+ * M % 256 == 0 and tokens_per_slot % 128 == 0 (else SF_ERR_PARAMETER). */
 int sf_block_tail(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
                   const float* b1, const float* b2, void* xres, void* xmod_out, const float* gate_msa,
                   const float* shift_mlp, const float* scale_mlp, const float* gate_mlp, const float* shift_next,
                   const float* scale_next, int64_t vec_stride, float ln_eps, int64_t M, int32_t tokens_per_slot,
                   void* stream);
-/* Experimental (slower): sf_block_tail that also computes the next layer's QKV
- * projection from the LayerNorm output it keeps in smem (q, k bf16 head-major, vt fp16). */
-int sf_block_tail_qkv(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
-                      const float* b1, const float* b2, void* xres, const float* gate_msa, const float* shift_mlp,
-                      const float* scale_mlp, const float* gate_mlp, const float* shift_next, const float* scale_next,
-                      int64_t vec_stride, float ln_eps, int64_t M, int32_t tokens_per_slot, const void* wqkv,
-                      const float* bqkv, void* q, void* k, void* vt, int32_t heads, float q_scale, void* stream);
 
 /* K6 -- flash attention, T tokens per row (multiple of 256), head dim 64, no mask.
  * q, k: [rows, heads, T, 64] bf16 (q pre-scaled), vt: [rows, heads, 64, T] fp16;

@@ -61,7 +61,6 @@ SIGNATURES = {
     "sf_attention_hd": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp],
     "sf_numpy_normal": [_vp, _i64, _i64, _i64, _vp, C.c_int, _vp],
     "sf_philox_normal": [_vp, _i64, _i64, C.c_uint64, _i64, _vp],
-    "sf_mlp_fused": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, _i64, _i32, _vp],
     "sf_block_tail": [_vp] * 15 + [_i64, C.c_float, _i64, _i32, _vp],
 }
 

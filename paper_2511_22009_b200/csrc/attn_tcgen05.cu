@@ -32,34 +32,8 @@
 #include "sf_internal.h"
 #include "sf_ptx.cuh"
 
-#ifndef SF_ATTN_NOEXP
-#define SF_ATTN_NOEXP 0  // diagnostics: 1 = skip exp2 (timing only, wrong results), 2 = all MUFU,
-                         // 3 = softmax skipped (MMA/sync skeleton), 4 = no MMAs
-#endif
-#ifndef SF_ATTN_WARP_ARRIVE
-#define SF_ATTN_WARP_ARRIVE 0  // 1: one P-ready arrival per warp (measured 259/305 vs 252/309 us: no gain)
-#endif
-#ifndef SF_ATTN_DEFER
-#define SF_ATTN_DEFER 0  // 1: signal P(j-1) after S(j) is loaded and reduced (measured slower: 256 vs 253 us)
-#endif
-#ifndef SF_ATTN_QTMEM
-#define SF_ATTN_QTMEM 1  // head dim 64: Q staged in TMEM (tcgen05.cp), S MMA in TS form
-#endif
 #ifndef SF_ATTN_TRACE
 #define SF_ATTN_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_attn_trace_read)
-#endif
-#ifndef SF_ATTN_SATCLAMP
-#define SF_ATTN_SATCLAMP 0  // 1: polynomial exp2 input clamped by a saturating FFMA (u = sat(x/256 + 127/256));
-                            // one issue slot less per pair but measured neutral (276.3 vs 276.4 us avg, E=5/6)
-#endif
-#ifndef SF_ATTN_MAX3
-#define SF_ATTN_MAX3 1  // row max as four 3-input max chains (32+2 FMNMX3) instead of 8 + 24 + 7 (276.4 vs 279.9 us)
-#endif
-#ifndef SF_ATTN_KV_STAGES
-#define SF_ATTN_KV_STAGES 6  // K/V^T ring depth (64-key stages of 18 KB at head dim 64)
-#endif
-#ifndef SF_ATTN_EMU_PAIRS
-#define SF_ATTN_EMU_PAIRS 6  // exp2 pairs per 32-key chunk evaluated by polynomial (of 16)
 #endif
 
 namespace sf {
@@ -79,7 +53,8 @@ __device__ long long g_attn_trace[16 * 64];
 namespace attn {
 constexpr int BQ = 128;  // queries per tile (2 tiles per item)
 constexpr int BKV = 64;  // keys per KV tile
-constexpr int KV_STAGES = SF_ATTN_KV_STAGES;
+constexpr int KV_STAGES = 6;  // K/V^T ring depth (64-key stages of 18 KB at head dim 64)
+constexpr int EMU_PAIRS = 6;  // exp2 pairs per 32-key chunk evaluated by the FMA-pipe polynomial (of 16)
 constexpr int QBUF = 2;
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int TMEM_COLS = 512;
@@ -151,31 +126,6 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__uint_as_float(b0), __uint_as_float(b1));
 }
 
-// Same, from raw scores s with the clamp folded into a saturating FFMA per element:
-// u = sat(s * L2E/256 + (127 - m)/256) is x = s*L2E - m clamped to [-127, 129] in units
-// of 1/256 (x <= 8 after the lazy-rescale check), x = 256u - 127 exactly enough
-// (abs. error 256 * 2^-25 in x, 1e-5 relative in 2^x); then
-//   t = 256u + (magic - 127) = magic + rint(x),  k' = (magic - 127) - t = -(rint(x) + 127),
-//   f = 256u + k' = x - rint(x):  11 issue slots per pair instead of 12.
-__device__ __forceinline__ float sat_fma(float a, float b, float c) {
-  float d;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-__device__ __forceinline__ float2 exp2_poly2_sat(float2 s, float a, float c) {
-  const float kMagic = 12582912.0f;
-  const float2 u = make_float2(sat_fma(s.x, a, c), sat_fma(s.y, a, c));
-  const float2 t = __ffma2_rn(u, make_float2(256.f, 256.f), make_float2(kMagic - 127.f, kMagic - 127.f));
-  const float2 kn = __ffma2_rn(t, make_float2(-1.f, -1.f), make_float2(kMagic - 127.f, kMagic - 127.f));
-  const float2 f = __ffma2_rn(u, make_float2(256.f, 256.f), kn);
-  float2 p = __ffma2_rn(f, make_float2(0.055088773f, 0.055088773f), make_float2(0.24260406f, 0.24260406f));
-  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
-  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
-  const uint32_t b0 = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
-  const uint32_t b1 = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
-  return make_float2(__uint_as_float(b0), __uint_as_float(b1));
-}
-
 // D[tmem] (+)= A[tmem] * B[smem]^T (A operand read from TMEM, "TS" form).
 // smem -> TMEM copy of a 128-row x 32-byte block described by an smem matrix descriptor.
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
@@ -200,7 +150,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
                      int nitems) {
   using namespace attn;
   using AC = AttnCfg<HD>;
-  constexpr bool Q_IN_TMEM = HD == 64 && SF_ATTN_QTMEM;
+  constexpr bool Q_IN_TMEM = HD == 64;  // Q staged in TMEM (tcgen05.cp), S MMA in TS form
   constexpr int Q_TILE = AC::Q_TILE, Q_BYTES = AC::Q_BYTES, K_BYTES = AC::K_BYTES, STAGE = AC::STAGE;
   constexpr int V_ROWS = AC::V_ROWS, V_TMA = AC::V_TMA;
   extern __shared__ uint8_t smem_raw[];
@@ -246,7 +196,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], SF_ATTN_WARP_ARRIVE ? 4 : 128);
+      mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
     }
     for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], 128);
@@ -265,7 +215,6 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  grid_dep_sync();
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 8) {
@@ -308,8 +257,7 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       const uint64_t qd = q_desc0 + (uint64_t)((qb * Q_BYTES) >> 4);
       const uint64_t kd = kv_desc0 + (uint64_t)((s * STAGE) >> 4);
       if (elect_one()) {
-        if constexpr (SF_ATTN_NOEXP == 4) {  // diagnostics: no MMAs (softmax/sync alone)
-        } else if constexpr (Q_IN_TMEM) {
+        if constexpr (Q_IN_TMEM) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) mma_f16_ts(tmem + S_COL(t, b), tmem + Q_COL(t) + 8 * k, kd + 2 * k, idesc_s, k != 0);
         } else {
@@ -328,7 +276,6 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          if (SF_ATTN_NOEXP != 4)
             mma_f16_ts(tmem + O_COL(t), tmem + P_COL(t, b) + 8 * k, vd + 2 * k, idesc_pv, acc || k != 0);
         mma_commit(&o_full[2 * t + b]);
         mma_commit(&kv_empty[s]);
@@ -397,17 +344,11 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         mbar_wait(&s_full[2 * t + b], (G >> 1) & 1);
         if (lane == 0 && quarter == 0) ATR(2 * t, G);
         tc_fence_after();
-#if SF_ATTN_NOEXP == 3  // diagnostics: softmax does no work (MMA/sync skeleton alone)
-        __syncwarp();
-        if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + b]);
-        continue;
-#endif
         float s[BKV];
         tmem_ld32(lane_base + S_COL(t, b), *reinterpret_cast<float(*)[32]>(&s[0]));
         tmem_ld32(lane_base + S_COL(t, b) + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
         tmem_ld_wait();
         if (lane == 0 && quarter == 0) ATR(8 + 4 * t, G);  // S in registers
-#if SF_ATTN_MAX3
         // four chains of 3-input maxima over 16 scores each (7 + 1 FMNMX3 per chain), then 4 -> 1
         float mx[4];
 #pragma unroll
@@ -419,25 +360,6 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], s[BKV - 4 + q]);
         const float m_tile = L2E * fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-#else
-        float mx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(s[i], s[i + 8]);
-#pragma unroll
-        for (int i = 16; i < BKV; i += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], fmaxf(s[i + q], s[i + 8 + q]));
-        const float m_tile = L2E * fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-#endif
-#if SF_ATTN_DEFER
-        if (j > 0) {  // P_t(j-1) (stored last iteration, its latency hidden behind this S load + max)
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + (b ^ 1)]);
-        }
-#endif
         if (j == 0) {
           m_ref = m_tile;
         } else {
@@ -462,7 +384,6 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
         }
         if (lane == 0 && quarter == 0) ATR(9 + 4 * t, G);  // max + rescale check done
         const float2 l2e2 = make_float2(L2E, L2E), negm = make_float2(-m_ref, -m_ref);
-        const float sat_c = (127.f - m_ref) * (1.f / 256.f);
 #pragma unroll
         for (int c = 0; c < BKV / 32; ++c) {
           uint32_t pk[16];
@@ -470,47 +391,23 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
           for (int i = 0; i < 16; ++i) {
             const float2 x = __ffma2_rn(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), l2e2, negm);
             float2 p;
-#if SF_ATTN_NOEXP == 1
-            p = x;  // diagnostics: no exponentials (timing only)
-#elif SF_ATTN_NOEXP == 2
-            p.x = ex2(x.x);
-            p.y = ex2(x.y);
-#else
-            if (i < SF_ATTN_EMU_PAIRS) {
-#if SF_ATTN_SATCLAMP
-              p = exp2_poly2_sat(make_float2(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]), L2E * (1.f / 256.f), sat_c);
-#else
+            if (i < attn::EMU_PAIRS) {
               p = exp2_poly2(x);
-#endif
             } else {
               p.x = ex2(x.x);
               p.y = ex2(x.y);
             }
-#endif
             pk[i] = pack_f16(p.x, p.y);
           }
           tmem_st16u(lane_base + P_COL(t, b) + 16 * c, pk);
         }
         if (lane == 0 && quarter == 0) ATR(10 + 4 * t, G);  // P computed, stores issued
-#if !SF_ATTN_DEFER
         tmem_st_wait();
         if (lane == 0 && quarter == 0) ATR(11 + 4 * t, G);  // stores complete
         tc_fence_before();
-#if SF_ATTN_WARP_ARRIVE
-        __syncwarp();  // the warp's P stores are complete: one arrival per warp
-        if (lane == 0) mbar_arrive(&p_full[2 * t + b]);
-#else
         mbar_arrive(&p_full[2 * t + b]);
-#endif
         if (lane == 0 && quarter == 0) ATR(2 * t + 1, G);
-#endif
       }
-#if SF_ATTN_DEFER
-      tmem_st_wait();  // the item's last P
-      tc_fence_before();
-      __syncwarp();
-      if (!SF_ATTN_WARP_ARRIVE || lane == 0) mbar_arrive(&p_full[2 * t + ((nkv - 1) & 1)]);
-#endif
       // epilogue: O / l -> bf16 -> out[row*T + q, head*HD ...]
       mbar_wait(&o_full[2 * t + 1], ((G - 1) >> 1) & 1);  // last PV (odd buffer); earlier PVs completed before it
       tc_fence_after();
@@ -586,10 +483,10 @@ int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, 
   const int grid = (int)(items < attn_sm_count() ? items : attn_sm_count());
   cudaError_t err;
   if (m.hd == 64)
-    err = launch_maybe_pdl(attn_fwd_tcgen05<64>, dim3(grid), dim3(attn::THREADS), AttnCfg<64>::SMEM, st, m.q, m.qh,
+    err = launch_kernel(attn_fwd_tcgen05<64>, dim3(grid), dim3(attn::THREADS), AttnCfg<64>::SMEM, st, m.q, m.qh,
                            m.k, m.kh, m.v, out, T, heads, (int)items);
   else if (m.hd == 72)
-    err = launch_maybe_pdl(attn_fwd_tcgen05<72>, dim3(grid), dim3(attn::THREADS), AttnCfg<72>::SMEM, st, m.q, m.qh,
+    err = launch_kernel(attn_fwd_tcgen05<72>, dim3(grid), dim3(attn::THREADS), AttnCfg<72>::SMEM, st, m.q, m.qh,
                            m.k, m.kh, m.v, out, T, heads, (int)items);
   else
     return SF_ERR_PARAMETER;

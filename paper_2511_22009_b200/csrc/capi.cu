@@ -15,26 +15,13 @@ int sf_device_sm_count(void) {
   return n;
 }
 
-// 2-SM (cta_group::2) pair tiles for the bf16/GELU (BN = 256) and QKV (head dim 64) GEMMs:
-// off by default (the single-CTA kernels are faster end to end: the pair main loop alone is
-// ~6% faster but the coupled epilogues lose more); sf_diag_gemm_2sm(1) selects them (diagnostics).
-static int g_gemm_2sm = 0;
-int sf_diag_gemm_2sm(int on) {
-  g_gemm_2sm = on;
-  return 0;
-}
-
 int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64_t M, int64_t N, int64_t K,
                  int32_t epi, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % 128) return SF_ERR_PARAMETER;
-  const int no_store = (epi & 0x200) ? 2 : (epi & 0x100) ? 1 : 0;  // diagnostics flags (not part of the documented ABI values)
-  epi &= 0xff;
   if (epi < EPI_F32 || epi > EPI_GELU) return SF_ERR_PARAMETER;
   const int bn = (N % 256 == 0) ? 256 : 128;
-  const bool two = g_gemm_2sm && bn == 256 && (epi == EPI_BF16 || epi == EPI_GELU);
   GemmMaps maps;
-  if ((two ? make_operand_maps_2sm(&maps, A, M, K, W, N, bn) : make_operand_maps(&maps, A, M, K, W, N, bn)) != SF_OK)
-    return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
   if (epi != EPI_F32 && (gemm_narrow_out(bn, epi) ? make_out_map32(&maps.d[0], C, M, N)
                                                   : make_out_map(&maps.d[0], C, M, N)) != SF_OK)
     return SF_ERR_CUDA;
@@ -44,8 +31,6 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   ep.ldo = N;
   ep.tokens_per_slot = 1 << 30;
   ep.M = (int)M;
-  ep.no_store = no_store;
-  if (two) return launch_gemm_2sm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
   return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
@@ -54,10 +39,8 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   const int bn = hd == 64 ? qkv_bn64() : 144;
   const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
   if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
-  const bool two = g_gemm_2sm && hd == 64 && bn == 192;
   GemmMaps maps;
-  if ((two ? make_operand_maps_2sm(&maps, A, M, K, W, N, bn) : make_operand_maps(&maps, A, M, K, W, N, bn)) != SF_OK)
-    return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
   if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
@@ -65,7 +48,6 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   ep.q_scale = q_scale;
   ep.tokens_per_slot = T;
   ep.M = (int)M;
-  if (two) return launch_gemm_2sm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
   return launch_gemm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }
 
@@ -97,21 +79,13 @@ int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float
                             tokens_per_slot, ln_eps, (cudaStream_t)stream);
 }
 
-// Diagnostics only (not in the header): 1 = skip epilogue stores, 2 = main loop only,
-// 3 / 4 = force the single-CTA 384-wide / the 2-CTA cluster RES_LN kernel.
-static int g_diag_res_ln = 0;
-int sf_diag_res_ln(int mode) {
-  g_diag_res_ln = mode;
-  return 0;
-}
-
 int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, void* xmod, const float* gate,
                    const float* shift, const float* scale, int64_t vec_stride, int64_t M, int64_t N, int64_t K,
                    int32_t tokens_per_slot, float ln_eps, void* stream) {
   if (N != 384 || K % 64 || M < 1 || M % tokens_per_slot || tokens_per_slot % 128) return SF_ERR_PARAMETER;
-  // 2-CTA cluster kernel (192-column slices, statistics exchanged through DSMEM) unless
-  // diagnostics ask for the single-CTA 384-wide tile (mode 3)
-  const bool cl = g_diag_res_ln == 4 || (g_diag_res_ln != 3 && K >= 1024);  // as the DiT runtime: cluster for long K
+  // long K: 2-CTA cluster kernel (192-column slices, statistics exchanged through DSMEM);
+  // short K: one CTA per 384-wide row tile (its short main loop does not amortise the exchange)
+  const bool cl = K >= 1024;
   GemmMaps maps;
   if (make_operand_maps(&maps, A, M, K, W, N, cl ? 192 : 384) != SF_OK) return SF_ERR_CUDA;
   if (make_out_map32(&maps.d[0], xres, M, N) != SF_OK || make_out_map32(&maps.d[1], xmod, M, N) != SF_OK)
@@ -126,7 +100,6 @@ int sf_gemm_res_ln(const void* A, const void* W, const float* bias, void* xres, 
   ep.ln_eps = ln_eps;
   ep.tokens_per_slot = tokens_per_slot;
   ep.M = (int)M;
-  ep.no_store = g_diag_res_ln >= 3 ? 0 : g_diag_res_ln;
   return cl ? launch_gemm(EPI_RES_LN2, 192, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream)
             : launch_gemm(EPI_RES_LN, 384, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
 }

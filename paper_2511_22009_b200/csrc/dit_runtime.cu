@@ -18,12 +18,6 @@
 #include "gemm_tcgen05.cuh"
 #include "sf_internal.h"
 
-#ifndef SF_FINAL_MMA
-#define SF_FINAL_MMA 1  // final layer on mma.sync (0: the per-lane FMA kernel)
-#endif
-#ifndef SF_PATCH_MMA
-#define SF_PATCH_MMA 1  // patch embed + LN1 on mma.sync (0: the per-lane FMA kernel)
-#endif
 
 namespace sf {
 
@@ -176,122 +170,6 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// ============================================================ K2+K4: patch embed + pos + LN1 modulate
-// One warp per group of TOK consecutive tokens (grid-stride); lane owns columns
-// 128u + 4 lane + {0..3}.  Weights live in smem transposed ([PK][HID]); each
-// float4 weight read serves all TOK tokens of the group.
-template <int HID>
-__global__ void __launch_bounds__(256) patch_embed_ln_kernel(
-    const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
-    const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
-    float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
-  constexpr int U = HID / 128;
-  constexpr int PK = 16;  // C * P * P (4 * 2 * 2), checked at create
-  constexpr int TOK = HID <= 384 ? 4 : 2;
-  extern __shared__ float swT[];  // [PK][HID]
-  for (int idx = threadIdx.x; idx < HID * PK; idx += blockDim.x) {
-    const int nn = idx / PK, k = idx % PK;  // pw is [HID][PK]
-    swT[k * HID + nn] = __bfloat162float(pw[idx]);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int gw = HW / P, T = gw * gw;
-  const int64_t groups = total_tokens / TOK;  // T % TOK == 0: a group never straddles latents
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
-    const int64_t tok0 = grp * TOK;
-    const int64_t ni = tok0 / T;
-    const int tau0 = (int)(tok0 % T);
-    const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
-    float v[TOK][PK];
-#pragma unroll
-    for (int t = 0; t < TOK; ++t) {
-      const int pi = (tau0 + t) / gw, pj = (tau0 + t) % gw;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const float2 t2 = *reinterpret_cast<const float2*>(xl + (int64_t)c * HW * HW + (pi * 2 + p) * HW + pj * 2);
-          v[t][(c * 2 + p) * 2 + 0] = t2.x;
-          v[t][(c * 2 + p) * 2 + 1] = t2.y;
-        }
-    }
-    // pass 1: residual y = patch . W + b + pos (bf16-rounded as stored) -> xres,
-    // row sums and sums of squares; pass 2 recomputes y (16 FMAs per element)
-    // for LayerNorm + modulate -> xmod.  Keeps the live set to one 128-column slice.
-    auto slice = [&](int u, float (&y)[TOK][4]) {
-      const int n0 = 128 * u + 4 * lane;
-      const float4 bb = *reinterpret_cast<const float4*>(pb + n0);
-#pragma unroll
-      for (int t = 0; t < TOK; ++t) {
-        const float4 pp = *reinterpret_cast<const float4*>(pos + (int64_t)(tau0 + t) * HID + n0);
-        y[t][0] = bb.x + pp.x;
-        y[t][1] = bb.y + pp.y;
-        y[t][2] = bb.z + pp.z;
-        y[t][3] = bb.w + pp.w;
-      }
-#pragma unroll
-      for (int k = 0; k < PK; ++k) {
-        const float4 wv = *reinterpret_cast<const float4*>(swT + k * HID + n0);
-#pragma unroll
-        for (int t = 0; t < TOK; ++t) {
-          y[t][0] += v[t][k] * wv.x;
-          y[t][1] += v[t][k] * wv.y;
-          y[t][2] += v[t][k] * wv.z;
-          y[t][3] += v[t][k] * wv.w;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < TOK; ++t)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) y[t][r] = __bfloat162float(__float2bfloat16_rn(y[t][r]));  // stored bf16
-    };
-    float sum[TOK], sq[TOK];
-#pragma unroll
-    for (int t = 0; t < TOK; ++t) sum[t] = sq[t] = 0.f;
-#pragma unroll 1
-    for (int u = 0; u < U; ++u) {
-      float y[TOK][4];
-      slice(u, y);
-#pragma unroll
-      for (int t = 0; t < TOK; ++t) {
-        *reinterpret_cast<uint2*>(xres + (tok0 + t) * HID + 128 * u + 4 * lane) =
-            make_uint2(pack_bf16(y[t][0], y[t][1]), pack_bf16(y[t][2], y[t][3]));
-        sum[t] += (y[t][0] + y[t][1]) + (y[t][2] + y[t][3]);
-        sq[t] += (y[t][0] * y[t][0] + y[t][1] * y[t][1]) + (y[t][2] * y[t][2] + y[t][3] * y[t][3]);
-      }
-    }
-    float mean[TOK], rstd[TOK];
-#pragma unroll
-    for (int t = 0; t < TOK; ++t) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        sum[t] += __shfl_xor_sync(0xffffffffu, sum[t], o);
-        sq[t] += __shfl_xor_sync(0xffffffffu, sq[t], o);
-      }
-      mean[t] = sum[t] / HID;
-      rstd[t] = rsqrtf(fmaxf(sq[t] / HID - mean[t] * mean[t], 0.f) + ln_eps);
-    }
-    const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
-    const float* scale = shift + HID;
-#pragma unroll 1
-    for (int u = 0; u < U; ++u) {
-      float y[TOK][4];
-      slice(u, y);
-      const int n0 = 128 * u + 4 * lane;
-      const float4 sh = *reinterpret_cast<const float4*>(shift + n0);
-      const float4 sc = *reinterpret_cast<const float4*>(scale + n0);
-#pragma unroll
-      for (int t = 0; t < TOK; ++t) {
-        const float o0 = (y[t][0] - mean[t]) * rstd[t] * (1.0f + sc.x) + sh.x;
-        const float o1 = (y[t][1] - mean[t]) * rstd[t] * (1.0f + sc.y) + sh.y;
-        const float o2 = (y[t][2] - mean[t]) * rstd[t] * (1.0f + sc.z) + sh.z;
-        const float o3 = (y[t][3] - mean[t]) * rstd[t] * (1.0f + sc.w) + sh.w;
-        *reinterpret_cast<uint2*>(xmod + (tok0 + t) * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
-      }
-    }
-  }
-}
 
 // The same patch embed + LN1 modulate on the warp-level tensor path (mma.sync
 // m16n8k16): one warp per 16 consecutive tokens, K = 16 = the patch vector
@@ -590,86 +468,6 @@ __device__ __forceinline__ void bfly_round(float (&a)[N], int o, int lane) {
   }
 }
 
-template <int HID, bool STREAM>
-__global__ void __launch_bounds__(256) final_layer_kernel(
-    const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
-    int P, int C, int64_t lat_rows,
-    // direct mode
-    float* __restrict__ eps_out,
-    // stream mode
-    const int64_t* __restrict__ ctl, int n, int64_t m, const double* __restrict__ stage_params,
-    const int64_t* __restrict__ row_info, int cfg, float w, float* __restrict__ x_ring,
-    const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
-    int64_t* __restrict__ frame_ids, int64_t total_tokens) {
-  constexpr int U = HID / 128;
-  constexpr int PK = 16;
-  constexpr int TOK = 4;
-  extern __shared__ float sw[];  // [PK][HID] + bias[PK]
-  for (int idx = threadIdx.x; idx < PK * HID; idx += blockDim.x) sw[idx] = __bfloat162float(fw[idx]);
-  for (int idx = threadIdx.x; idx < PK; idx += blockDim.x) sw[PK * HID + idx] = fb[idx];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int gw = HW / P, T = gw * gw;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  int64_t j = 0;
-  if constexpr (STREAM) j = ctl[1];
-  const int my_t = lane >> 3, my_f = 2 * (lane & 7);  // after the reduce-scatter
-
-  // eps (pre-CFG) of features my_f, my_f+1 of token tau0 + my_t of network row net_row
-  auto project = [&](int64_t net_row, int tau0) -> float2 {
-    float a[TOK * PK];
-#pragma unroll
-    for (int i = 0; i < TOK * PK; ++i) a[i] = 0.f;
-#pragma unroll 1
-    for (int u = 0; u < U; ++u) {
-      float xv[TOK][4];
-#pragma unroll
-      for (int t = 0; t < TOK; ++t) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(xmod + (net_row * T + tau0 + t) * HID + 128 * u + 4 * lane);
-        const float2 p0 = unpack_bf16(raw.x), p1 = unpack_bf16(raw.y);
-        xv[t][0] = p0.x;
-        xv[t][1] = p0.y;
-        xv[t][2] = p1.x;
-        xv[t][3] = p1.y;
-      }
-#pragma unroll
-      for (int f = 0; f < PK; ++f) {
-        const float4 wv = *reinterpret_cast<const float4*>(sw + f * HID + 128 * u + 4 * lane);
-#pragma unroll
-        for (int t = 0; t < TOK; ++t)
-          a[t * PK + f] += xv[t][0] * wv.x + xv[t][1] * wv.y + xv[t][2] * wv.z + xv[t][3] * wv.w;
-      }
-    }
-    // butterfly reduce-scatter over the 64 (token, feature) partials
-    bfly_round<32>(a, 16, lane);
-    bfly_round<16>(a, 8, lane);
-    bfly_round<8>(a, 4, lane);
-    bfly_round<4>(a, 2, lane);
-    bfly_round<2>(a, 1, lane);
-    return make_float2(a[0] + sw[PK * HID + my_f], a[1] + sw[PK * HID + my_f + 1]);
-  };
-
-  const int64_t groups = total_tokens / TOK;
-  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
-    const int64_t tok0 = grp * TOK;
-    const int64_t lr = tok0 / T;
-    const int tau0 = (int)(tok0 % T);
-    float2 e2 = project(STREAM && cfg ? lr + lat_rows : lr, tau0);
-    if constexpr (STREAM) {
-      if (cfg) {
-        const float2 eu = project(lr, tau0);
-        e2.x = __fadd_rn(eu.x, __fmul_rn(w, __fsub_rn(e2.x, eu.x)));  // handle_cfg (models.py:288-293)
-        e2.y = __fadd_rn(eu.y, __fmul_rn(w, __fsub_rn(e2.y, eu.y)));
-      }
-    }
-    const int tau = tau0 + my_t;
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      final_element<STREAM>(FinalOut{HW, P, C, eps_out, ctl, n, m, stage_params, row_info, x_ring, noise_in,
-                                     noise_seed, frames_out, frame_ids},
-                            j, lr, tau, gw, my_f + h, h ? e2.y : e2.x);
-  }
-}
 
 // Same layer on the warp-level tensor path (mma.sync m16n8k16, bf16 in, fp32
 // accumulate): one warp per 16 consecutive tokens (T % 16 == 0), N = 16 output
@@ -848,46 +646,13 @@ static int64_t ws_layout(const sf_dit_config& c, int64_t rows, int64_t* off /*[1
   take(5, M * H * 2);                 // k
   take(6, M * H * 2);                 // vt
   take(7, M * H * 2);                 // attn out
-  take(8, M * (int64_t)c.mlp_hidden * 2);  // mlp hidden
+  take(8, c.hidden == 384 ? 0 : M * (int64_t)c.mlp_hidden * 2);  // MLP hidden (the DiT-S/2 block tail keeps it on chip)
   take(9, rows * H * 4);                   // conditioning MLP hidden (fp32)
   return o;
 }
 
 // Kernel classes for per-launch profiling (sf_dit_profile_step).
-// Fused MLP block for the DiT-S/2 geometry (sf_diag_mlp_fused(0) restores the fc1 / fc2 GEMM pair).
-static int g_mlp_fused = -1;  // -1: from the environment (SF_MLP_FUSED=0 disables), default on
-static bool mlp_fused_ok(const sf_dit_config& c) {
-  if (g_mlp_fused < 0) {
-    const char* e = getenv("SF_MLP_FUSED");
-    g_mlp_fused = (e && e[0] == '0') ? 0 : 1;
-  }
-  return g_mlp_fused && c.hidden == 384 && c.mlp_hidden == 1536;
-}
-
-// Projection + MLP in one kernel (SF_BLOCK_TAIL=0 restores proj GEMM + fused MLP): standalone
-// no faster, but ~2% in the power-capped step (less DRAM traffic -> higher SM clock).
-static int g_block_tail = -1;
-static bool block_tail_ok(const sf_dit_config& c) {
-  if (g_block_tail < 0) {
-    const char* e = getenv("SF_BLOCK_TAIL");
-    g_block_tail = (e && e[0] == '0') ? 0 : 1;
-  }
-  return g_block_tail && mlp_fused_ok(c);
-}
-
-// The next layer's QKV projection at the end of the block tail (SF_TAIL_QKV=1; correct but
-// measured slower: 2833 vs 3019 frames/s -- the QKV phase serialises behind the tile's X buffer).
-static int g_tail_qkv = -1;
-static bool tail_qkv_ok() {
-  if (g_tail_qkv < 0) {
-    const char* e = getenv("SF_TAIL_QKV");
-    g_tail_qkv = (e && e[0] == '1') ? 1 : 0;
-  }
-  return g_tail_qkv;
-}
-
-enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_MLP, P_TAIL,
-                 P_NCLS };
+enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ, P_FC1, P_FC2, P_FINAL, P_TAIL, P_NCLS };
 
 // Called after every launch: counts launches and, in a profiled step, records
 // a CUDA event so each launch's duration can be attributed to its class.
@@ -925,14 +690,9 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
   const int H = c.hidden, T = h->tokens, hd = H / c.heads;
   const int64_t M = rows * T;
   const int64_t B6 = 6 * (int64_t)H;
-  // hidden 384: the 384-wide row fits one TMEM tile, so the gated residual and the
-  // next LayerNorm + modulate run in the GEMM epilogue (RES_LN).  Wider rows
-  // (DiT-XL, 1152): gated-residual epilogue (RES) + a LayerNorm/modulate pass.
-  const bool fused_ln = H == 384;
   int rc;
-  const bool tail_qkv = block_tail_ok(c) && tail_qkv_ok();
   for (int l = 0; l < c.depth; ++l) {
-    if (!(tail_qkv && l > 0)) {  // with tail_qkv, layer l's QKV ran in layer l-1's block tail
+    {
       EpiParams ep{};
       ep.bias = h->w.qkv_b + (int64_t)l * 3 * H;
       ep.heads = c.heads;
@@ -944,38 +704,27 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
     mark(h, P_ATTN, st);
-    if (block_tail_ok(c)) {
-      // projection + LN + MLP + next LN in one kernel (csrc/block_tail.cu)
-      const float* nxt = l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6;
-      const float* mb = h->mod + l * B6;
+    // LayerNorm modulate for what follows the block: the next block (shift_msa, scale_msa) or
+    // the final layer (shift, scale)
+    const float* nxt = l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6;
+    const float* mb = h->mod + l * B6;
+    if (H == 384) {
+      // DiT-S/2: projection + gated residual + LN + MLP + gated residual + next LN in one
+      // kernel on CTA pairs (csrc/block_tail.cu)
       if ((rc = launch_block_tail(h->attn, (const __nv_bfloat16*)h->w.proj_w + (int64_t)l * H * H,
                                   h->w.proj_b + (int64_t)l * H,
                                   (const __nv_bfloat16*)h->w.fc1_w + (int64_t)l * c.mlp_hidden * H,
                                   (const __nv_bfloat16*)h->w.fc2_w + (int64_t)l * H * c.mlp_hidden,
                                   h->w.fc1_b + (int64_t)l * c.mlp_hidden, h->w.fc2_b + (int64_t)l * H, h->xres,
                                   h->xmod, mb + 2 * H, mb + 3 * H, mb + 4 * H, mb + 5 * H, nxt, nxt + H,
-                                  h->mod_stride, c.ln_eps, M, T, st,
-                                  tail_qkv && l + 1 < c.depth
-                                      ? (const __nv_bfloat16*)h->w.qkv_w + (int64_t)(l + 1) * 3 * H * H
-                                      : nullptr,
-                                  h->w.qkv_b + (int64_t)(l + 1 < c.depth ? l + 1 : l) * 3 * H, h->q, h->k, h->vt,
-                                  c.heads, 1.0f / sqrtf((float)hd))))
+                                  h->mod_stride, c.ln_eps, M, T, st)))
         return rc;
       mark(h, P_TAIL, st);
       continue;
     }
+    // DiT-XL/2 (1152-wide rows): gated-residual GEMM epilogues (128-wide tiles) + a LayerNorm /
+    // modulate pass, with fc1 + GELU in between
     for (int half = 0; half < 2; ++half) {  // 0: attention proj (gate_msa), 1: MLP (fc1 + GELU, fc2, gate_mlp)
-      if (half == 1 && mlp_fused_ok(c)) {
-        // DiT-S/2: the whole MLP block in one kernel (hidden kept on chip, csrc/mlp_fused.cu)
-        const float* nxt = l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6;
-        if ((rc = launch_mlp_fused(h->xmod, (const __nv_bfloat16*)h->w.fc1_w + (int64_t)l * c.mlp_hidden * H,
-                                   (const __nv_bfloat16*)h->w.fc2_w + (int64_t)l * H * c.mlp_hidden,
-                                   h->w.fc1_b + (int64_t)l * c.mlp_hidden, h->w.fc2_b + (int64_t)l * H, h->xres,
-                                   h->xmod, h->mod + l * B6 + 5 * H, nxt, nxt + H, h->mod_stride, c.ln_eps, M, T, st)))
-          return rc;
-        mark(h, P_MLP, st);
-        continue;
-      }
       if (half == 1) {
         EpiParams ep{};
         ep.bias = h->w.fc1_b + (int64_t)l * c.mlp_hidden;
@@ -991,34 +740,15 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       EpiParams ep{};
       ep.bias = (half == 0 ? h->w.proj_b : h->w.fc2_b) + (int64_t)l * H;
       ep.xres = h->xres;
-      ep.gate = h->mod + l * B6 + (half == 0 ? 2 : 5) * H;  // gate_msa / gate_mlp
-      // LayerNorm modulate for what comes next: the MLP (shift_mlp, scale_mlp), the
-      // next block (shift_msa, scale_msa) or the final layer (shift, scale)
-      const float* nxt = half == 0 ? h->mod + l * B6 + 3 * H
-                                   : (l + 1 < c.depth ? h->mod + (l + 1) * B6 : h->mod + c.depth * B6);
-      ep.shift = nxt;
-      ep.scale = nxt + H;
+      ep.gate = mb + (half == 0 ? 2 : 5) * H;  // gate_msa / gate_mlp
       ep.vec_stride = h->mod_stride;
-      ep.ln_eps = c.ln_eps;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if (fused_ln) {
-        // fc2 (K = 1536): 2-CTA cluster kernel (192-column slices, double-buffered
-        // accumulators, LayerNorm statistics through DSMEM); proj (K = 384): one CTA
-        // per 384-wide row tile (its short main loop does not amortise the exchange)
-        if (half == 1) {
-          if ((rc = launch_gemm(EPI_RES_LN2, 192, gm, (int)M, H, K, ep, st))) return rc;
-        } else {
-          if ((rc = launch_gemm(EPI_RES_LN, 384, gm, (int)M, H, K, ep, st))) return rc;
-        }
-        mark(h, cls, st);
-      } else {
-        if ((rc = launch_gemm(EPI_RES, 128, gm, (int)M, H, K, ep, st))) return rc;
-        mark(h, cls, st);
-        if ((rc = launch_ln_modulate(h->xres, h->xmod, nxt, nxt + H, h->mod_stride, M, H, T, c.ln_eps, st)))
-          return rc;
-        mark(h, cls, st);
-      }
+      if ((rc = launch_gemm(EPI_RES, 128, gm, (int)M, H, K, ep, st))) return rc;
+      mark(h, cls, st);
+      const float* ln = half == 0 ? mb + 3 * H : nxt;  // the MLP's (shift_mlp, scale_mlp) / what follows
+      if ((rc = launch_ln_modulate(h->xres, h->xmod, ln, ln + H, h->mod_stride, M, H, T, c.ln_eps, st))) return rc;
+      mark(h, cls, st);
     }
   }
   return SF_OK;
@@ -1041,31 +771,19 @@ static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t 
 static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const int64_t tokens = rows * h->tokens;
-#if SF_PATCH_MMA
   const size_t sm = c.hidden == 384 ? PatchMma<384>::SMEM : PatchMma<1152>::SMEM;
   const int wpb = c.hidden == 384 ? PatchMma<384>::WARPS : PatchMma<1152>::WARPS;
   // persistent: as many CTAs as fit (smem-limited: 2 per SM at hidden 384, 1 at 1152), each warp
   // walks several 16-token groups, so the B-fragment fill is paid once per CTA
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, c.hidden == 384 ? 2 * 148 : 148);
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
-#else
-  const size_t sm = (size_t)c.hidden * c.in_ch * c.patch * c.patch * sizeof(float);
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8);
-  auto kern = c.hidden == 384 ? patch_embed_ln_kernel<384> : patch_embed_ln_kernel<1152>;
-  const int wpb = 8;
-#endif
   kern<<<blocks, 32 * wpb, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
                                 h->w.patch_b, h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens);
   mark(h, P_PATCH, st);
   return cuda_status();
 }
 
-static size_t final_smem(const sf_dit_config& c) {
-  const int PK = c.in_ch * c.patch * c.patch;
-  return (size_t)(PK * c.hidden + PK) * sizeof(float);
-}
-
-// Final layer + Euler/emit/refill: the mma.sync kernel (default) or the FMA kernel (SF_FINAL_MMA=0).
+// Final layer + Euler/emit/refill (mma.sync kernel).
 template <bool STREAM>
 static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int64_t* ctl, int n, int64_t m,
                          const double* stage_params, const int64_t* row_info, int cfg, float w, float* x_ring,
@@ -1073,16 +791,10 @@ static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int6
                          int64_t tokens, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const __nv_bfloat16* fw = (const __nv_bfloat16*)h->w.final_w;
-#if SF_FINAL_MMA
   const int PK = c.in_ch * c.patch * c.patch;
   const size_t sm = (size_t)PK * (c.hidden * 2 + FINAL_WPAD) + PK * sizeof(float);
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + 7) / 8, 148 * 8);
   auto fk = c.hidden == 384 ? final_layer_mma_kernel<384, STREAM> : final_layer_mma_kernel<1152, STREAM>;
-#else
-  const size_t sm = final_smem(c);
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens + 31) / 32, 148 * 8);
-  auto fk = c.hidden == 384 ? final_layer_kernel<384, STREAM> : final_layer_kernel<1152, STREAM>;
-#endif
   fk<<<blocks, 256, sm, st>>>(h->xmod, fw, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
                               stage_params, row_info, cfg, w, x_ring, noise_in, noise_seed, frames_out, frame_ids,
                               tokens);
@@ -1141,16 +853,9 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     const int hd = H / c.heads;
     rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? qkv_bn64() : 144);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
-    rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
-    rc |= make_out_map32(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);  // 256-wide GELU tiles: 32-column chunks
-    if (H == 384) {  // RES_LN epilogue: whole rows per tile
-      rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 384);
-      rc |= make_out_map32(&h->g_proj[l].d[0], h->xres, M, H);
-      rc |= make_out_map32(&h->g_proj[l].d[1], h->xmod, M, H);
-      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 192);
-      rc |= make_out_map32(&h->g_fc2[l].d[0], h->xres, M, H);
-      rc |= make_out_map32(&h->g_fc2[l].d[1], h->xmod, M, H);
-    } else {  // RES epilogue (128-wide tiles) + LayerNorm pass
+    if (H != 384) {  // DiT-XL/2 MLP + projection as GEMMs: RES epilogue (128-wide tiles) + LayerNorm pass
+      rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
+      rc |= make_out_map32(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);  // 256-wide GELU tiles: 32-column chunks
       rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 128);
       rc |= make_out_map(&h->g_proj[l].d[0], h->xres, M, H);
       rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 128);
@@ -1167,17 +872,10 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     delete h;
     return SF_ERR_CUDA;
   }
-  const int psm = (int)(H * c.in_ch * c.patch * c.patch * sizeof(float)), fsm = (int)final_smem(c);
-  cudaFuncSetAttribute(patch_embed_ln_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
-  cudaFuncSetAttribute(patch_embed_ln_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
   cudaFuncSetAttribute(patch_embed_ln_mma_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        PatchMma<384>::SMEM);
   cudaFuncSetAttribute(patch_embed_ln_mma_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        PatchMma<1152>::SMEM);
-  cudaFuncSetAttribute(final_layer_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
-  cudaFuncSetAttribute(final_layer_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
-  cudaFuncSetAttribute(final_layer_kernel<1152, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
-  cudaFuncSetAttribute(final_layer_kernel<1152, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   *out = h;
   return cuda_status();
 }
@@ -1342,7 +1040,6 @@ int sf_philox_normal(float* out, int64_t S, int64_t D, uint64_t seed, int64_t ge
   return cuda_status();
 }
 
-void sf_diag_mlp_fused(int on) { g_mlp_fused = on; }
 
 int sf_dit_mod_stride(const sf_dit_config* c) { return c->depth * 6 * c->hidden + 2 * c->hidden; }
 

@@ -47,12 +47,6 @@ int gemm_bk(int bn) { return bn > 256 ? 32 : 64; }
 int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
 
 // 2-SM pair tiles: each CTA loads BN/2 rows of W per stage.
-int make_operand_maps_2sm(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
-  const int bk = gemm_bk(bn);
-  int rc = make_tmap_bf16_2d(&m->a, A, K, M, K, bk, 128, 2 * bk);
-  rc |= make_tmap_bf16_2d(&m->b, W, K, N, K, bk, bn / 2, 2 * bk);
-  return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
-}
 
 int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
   const int bk = gemm_bk(bn);
@@ -93,24 +87,13 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
-// QKV tile width for head dim 64 (192: 4 epilogue warps, 3 heads per tile; 128: 8 warps,
-// 2 heads); SF_QKV_BN in the environment overrides for experiments.
-int qkv_bn64() {
-  static int bn = 0;
-  if (!bn) {
-    const char* e = getenv("SF_QKV_BN");
-    bn = (e && atoi(e) == 128) ? 128 : 192;
-  }
-  return bn;
-}
+// QKV tile width for head dim 64: 192 columns (3 heads per tile, 4 epilogue warps).
+int qkv_bn64() { return 192; }
 
-#ifndef SF_QKV_WARPS
-#define SF_QKV_WARPS 4  // epilogue warps of the head-dim-64 QKV GEMM (4 or 12)
-#endif
 template <int BN, int KIND>
 constexpr int epi_warps() {
   // QKV: 4; RES_LN: 12; bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
-  return KIND == EPI_QKV ? (BN == 192 ? SF_QKV_WARPS : BN == 128 ? 8 : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+  return KIND == EPI_QKV ? (BN == 192 ? 4 : BN == 128 ? 8 : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
 }
 
 // Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).
@@ -135,22 +118,6 @@ static int set_attr() {
   return SF_OK;
 }
 
-template <int BN, int KIND>
-static int set_attr_2sm() {
-  static bool done = false;
-  if (!done) {
-    constexpr int W = epi_warps<BN, KIND>();
-    const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W, 2>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 GemmCfg<BN, W, KIND, 2>::SMEM_BYTES);
-    if (err != cudaSuccess) {
-      fprintf(stderr, "streamflow: gemm2sm<%d,%d> smem attribute failed: %s\n", BN, KIND, cudaGetErrorString(err));
-      return SF_ERR_CUDA;
-    }
-    done = true;
-  }
-  return SF_OK;
-}
 
 // Set every instantiation's smem attribute up front (never inside a graph capture).
 int prepare_gemm_kernels() {
@@ -167,20 +134,9 @@ int prepare_gemm_kernels() {
   rc |= set_attr<144, EPI_QKV>();
   rc |= set_attr<128, EPI_RES>();
   rc |= set_attr<192, EPI_RES_LN2>();
-  rc |= set_attr_2sm<256, EPI_GELU>();
-  rc |= set_attr_2sm<256, EPI_BF16>();
-  rc |= set_attr_2sm<192, EPI_QKV>();
   return rc;
 }
 
-bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SF_PDL");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on;
-}
 
 static int sm_count() {
   static int n = 0;
@@ -222,7 +178,7 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
     err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W>, maps, N, K, e);
     if (err == cudaSuccess) err = cudaGetLastError();
   } else {
-    err = launch_maybe_pdl(gemm_bf16_tcgen05<BN, KIND, W>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, maps, N,
+    err = launch_kernel(gemm_bf16_tcgen05<BN, KIND, W>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, maps, N,
                            K, e);
     if (err == cudaSuccess) err = cudaGetLastError();
   }
@@ -234,45 +190,7 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
   return SF_OK;
 }
 
-template <int BN, int KIND>
-static int launch_one_2sm(const GemmMaps& maps, int M, int N, int K, const EpiParams& ep, cudaStream_t st) {
-  constexpr int W = epi_warps<BN, KIND>();
-  using C = GemmCfg<BN, W, KIND, 2>;
-  if (K % C::BK) return SF_ERR_PARAMETER;
-  if (set_attr_2sm<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
-  const int pairs = ((M + C::BM - 1) / C::BM + 1) / 2 * (N / BN), max_cl = sm_count() / 2;
-  EpiParams e = ep;
-  e.M = M;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * (pairs < max_cl ? pairs : max_cl)));
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W, 2>, maps, N, K, e);
-  if (err == cudaSuccess) err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    fprintf(stderr, "streamflow: gemm2sm<%d,%d> launch failed: %s\n", BN, KIND, cudaGetErrorString(err));
-    return SF_ERR_CUDA;
-  }
-  return SF_OK;
-}
 
-// 2-SM (cta_group::2) pair tiles 256 x bn; maps from make_operand_maps_2sm.
-int launch_gemm_2sm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
-                    cudaStream_t st) {
-  if (K % 64 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
-  if (bn == 256 && kind == EPI_GELU) return launch_one_2sm<256, EPI_GELU>(maps, M, N, K, ep, st);
-  if (bn == 256 && kind == EPI_BF16) return launch_one_2sm<256, EPI_BF16>(maps, M, N, K, ep, st);
-  if (bn == 192 && kind == EPI_QKV) return launch_one_2sm<192, EPI_QKV>(maps, M, N, K, ep, st);
-  return SF_ERR_PARAMETER;
-}
 
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
                 cudaStream_t st) {

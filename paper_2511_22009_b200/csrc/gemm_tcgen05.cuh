@@ -20,9 +20,6 @@
 
 namespace sf {
 
-#ifndef SF_GEMM_L2HINT
-#define SF_GEMM_L2HINT 0  // experiment: evict-first output stores, evict-last weight loads
-#endif
 #ifndef SF_GEMM_TRACE
 #define SF_GEMM_TRACE 0  // diagnostics: clock64 timeline of CTA 0 (sf_gemm_trace_read)
 #endif
@@ -38,21 +35,6 @@ __device__ long long g_gemm_trace[8 * 64];
   } while (0)
 #endif
 
-#ifndef SF_QKV_DIAG_NOVT
-#define SF_QKV_DIAG_NOVT 0
-#endif
-#ifndef SF_QKV_BIAS_ALL
-#define SF_QKV_BIAS_ALL 1  // QKV epilogue: whole bias staged in smem once per CTA
-#endif
-#ifndef SF_QKV_NBUF
-#define SF_QKV_NBUF 3  // QKV epilogue: TMA-store staging buffers per warp (3: 118.7 vs 122.1 us, 4: 128.5 -- one A/B stage fewer)
-#endif
-#ifndef SF_QKV_VT_PAIR
-#define SF_QKV_VT_PAIR 1  // QKV epilogue: V^T staged as 4-byte token pairs (lane-pair shuffle)
-#endif
-#ifndef SF_QKV_LD64
-#define SF_QKV_LD64 1  // QKV epilogue: one TMEM-load wait per 64-column head chunk
-#endif
 enum EpiKind : int {
   EPI_F32 = 0,     // out f32 [M, ldo]  = acc + bias
   EPI_BF16 = 1,    // out bf16 [M, ldo] = acc + bias
@@ -82,7 +64,6 @@ struct EpiParams {
   // common
   int tokens_per_slot;  // rows of one latent (1024); tiles never straddle a slot
   int M;                // valid rows (tail rows of the last tile are masked)
-  int no_store;         // diagnostics only: skip the epilogue's global stores
 };
 
 // TMA descriptors: A, B operands and up to three outputs
@@ -124,8 +105,8 @@ struct GemmCfg {
   static constexpr bool LN_RING = KIND == EPI_RES_LN || KIND == EPI_RES_LN2;  // 32-column SW64 chunks
   static constexpr bool NARROW = LN_RING || ((KIND == EPI_BF16 || KIND == EPI_GELU) && EPI_WARPS == 16);
   static constexpr int OUT_BUF = BN == 144 ? 5120 : NARROW ? 2048 : 4096;
-  // RES_LN(2): one buffer per chunk; QKV (head dim 64): SF_QKV_NBUF store buffers per warp
-  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : (KIND == EPI_QKV && BN == 192) ? SF_QKV_NBUF : 2;
+  // RES_LN(2): one buffer per chunk; QKV (head dim 64): 3 store buffers per warp
+  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : (KIND == EPI_QKV && BN == 192) ? 3 : 2;
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
   static constexpr int RBAR_BYTES = EPI_WARPS * 4 * 8;  // residual-chunk barriers (one per staging buffer)
   // RES_LN2 exchange: [tile parity][pass][source CTA][column group][128 rows] floats
@@ -198,11 +179,7 @@ struct OutStageT {
     __syncwarp();
     if (lane == 0) {
       if (store) {
-#if SF_GEMM_L2HINT
-        tma_store_2d_hint(map, buf, c0, c1, l2_policy_evict_first());
-#else
         tma_store_2d(map, buf, c0, c1);
-#endif
       }
       bulk_commit();
     }
@@ -290,7 +267,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  grid_dep_sync();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
@@ -314,13 +290,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           tma_load_2d(sA + s * C::A_BYTES, &maps.a, &full[s], kb * C::BK, m0);
 #pragma unroll
           for (int h = 0; h < BN / C::B_BOX; ++h) {
-#if SF_GEMM_L2HINT
-            tma_load_2d_hint(sB + s * C::B_BYTES + h * C::B_BOX * C::SWZ, &maps.b, &full[s], kb * C::BK,
-                             n0 + h * C::B_BOX, l2_policy_evict_last());
-#else
             tma_load_2d(sB + s * C::B_BYTES + h * C::B_BOX * C::SWZ, &maps.b, &full[s], kb * C::BK,
                         n0 + h * C::B_BOX);
-#endif
           }
         }
       }
@@ -379,12 +350,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     using OutStage = OutStageT<C::OUT_BUF, C::LN_RING ? 2 : C::OUT_NBUF>;
     OutStage out{sOut + e * C::OUT_NBUF * C::OUT_BUF, 0};
     uint32_t ring = 0;  // RES: per-buffer load parity bits
-    const bool do_store = !ep.no_store;
     uint32_t local = 0;
     // QKV: the whole bias row (3*hidden floats) fits the vector area, so it is staged
     // once instead of per tile (the per-tile global-load latency sat on the epilogue's
     // critical path, which bounds this GEMM: ~4400 vs ~2900 MMA cycles per tile)
-    const bool bias_all = KIND == EPI_QKV && SF_QKV_BIAS_ALL && N * 4 <= C::VEC_BYTES;
+    const bool bias_all = KIND == EPI_QKV && N * 4 <= C::VEC_BYTES;
     if (bias_all) {
       for (int c = et; c < N; c += EPI_THREADS) vecs[c] = ep.bias[c];
       named_bar_sync(5, EPI_THREADS);
@@ -449,10 +419,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (warp == 2 && lane == 0) GTR(3, local);
-      if (ep.no_store == 2) {  // diagnostics: main loop only
-        acc_release(acc);
-        continue;
-      }
       const float* vbias = bias_all ? vecs + n0 + c_lo : vb + c_lo;
 
       if constexpr (KIND == EPI_F32) {
@@ -461,7 +427,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           float v[32];
           tmem_ld32(taddr + c_lo + c0, v);
           tmem_ld_wait();
-          if (valid && do_store) {
+          if (valid) {
             float4* dst =
                 reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + n0 + c_lo + c0);
 #pragma unroll
@@ -494,14 +460,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, i, pack8_bf16(v + 8 * i));
-          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
+          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_BF16 || KIND == EPI_GELU) {
 #pragma unroll 1
         for (int c0 = 0; c0 < COLS; c0 += 64) {
           uint8_t* buf = out.acquire(lane);
           if (warp == 2 && lane == 0) GTR(4, 3 * local + c0 / 64);
-#if SF_QKV_LD64
           // both 32-column halves of the head in flight before one wait; the
           // accumulator is released as soon as the tile's last columns are in registers
           float v64[64];
@@ -510,16 +475,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           tmem_ld_wait();
           if (warp == 2 && lane == 0) GTR(5, 3 * local + c0 / 64);
           if (c0 + 64 >= COLS) acc_release(acc);
-#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-#if SF_QKV_LD64
             float* v = v64 + 32 * h;
-#else
-            float v[32];
-            tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
-            tmem_ld_wait();
-#endif
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
@@ -538,7 +496,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           if (c0 + 64 >= COLS) {  // last TMEM read of this tile by this warp
             acc_release(acc);
           }
-          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, do_store && r0 < ep.M);
+          out.release(lane, &maps.d[0], buf, n0 + c_lo + c0, r0, r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_QKV && BN == 144) {
         // head dim 72: a 144-column tile = two whole heads of one of Q / K / V.
@@ -580,14 +538,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
               *reinterpret_cast<__half*>(buf + i * 64 + ((((lane >> 3) ^ ((i >> 1) & 3))) * 16) + (lane & 7) * 2) =
                   __float2half_rn(v[i]);
           }
-          if (which < 2 || SF_QKV_DIAG_NOVT)
-            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          if (which < 2)
+            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), r0 < ep.M);
           else
-            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 72), do_store && r0 < ep.M);
+            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 72), r0 < ep.M);
         }
       } else if constexpr (KIND == EPI_RES) {
         const float* vgate = vb + BN + c_lo;
-        const bool st_ok = do_store && r0 < ep.M;
+        const bool st_ok = r0 < ep.M;
 #pragma unroll 1
         for (int c = 0; c < COLS / 64; ++c) {
           uint8_t* buf = rbuf0 + c * 4096;
@@ -620,11 +578,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           __syncwarp();
           if (lane == 0) {
             if (st_ok) {
-#if SF_GEMM_L2HINT
-              tma_store_2d_hint(&maps.d[0], buf, n0 + c_lo + 64 * c, r0, l2_policy_evict_first());
-#else
               tma_store_2d(&maps.d[0], buf, n0 + c_lo + 64 * c, r0);
-#endif
             }
             bulk_commit();
           }
@@ -645,7 +599,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           const float sc = which == 0 ? ep.q_scale : 1.0f;
           uint8_t* buf = out.acquire(lane);
           if (warp == 2 && lane == 0) GTR(4, 3 * local + c0 / 64);
-#if SF_QKV_LD64
           // both 32-column halves of the head in flight before one wait; the
           // accumulator is released as soon as the tile's last columns are in registers
           float v64[64];
@@ -654,16 +607,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
           tmem_ld_wait();
           if (warp == 2 && lane == 0) GTR(5, 3 * local + c0 / 64);
           if (c0 + 64 >= COLS) acc_release(acc);
-#endif
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-#if SF_QKV_LD64
             float* v = v64 + 32 * h;
-#else
-            float v[32];
-            tmem_ld32(taddr + c_lo + c0 + 32 * h, v);
-            tmem_ld_wait();
-#endif
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float4 b = reinterpret_cast<const float4*>(vbias + c0 + 32 * h)[i];
@@ -672,13 +618,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
               v[4 * i + 2] = (v[4 * i + 2] + b.z) * sc;
               v[4 * i + 3] = (v[4 * i + 3] + b.w) * sc;
             }
-            if (which < 2 || SF_QKV_DIAG_NOVT) {  // (diagnostic: V stored like K, timing only)
+            if (which < 2) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) OutStage::put16(buf, lane, 4 * h + i, pack8_bf16(v + 8 * i));
             } else {
               // V^T staging: 64 rows (head dim) x 64 B (32 tokens), 64B swizzle:
               // 16-byte chunk c of row dd lives at chunk c ^ ((dd >> 1) & 3)
-#if SF_QKV_VT_PAIR
               // dims (2p, 2p+1) x tokens (2j, 2j+1) are swapped across lane pairs with one
               // shuffle, so each lane stores a 4-byte token pair: 16 STS.32 (1 wavefront
               // each: the two rows are adjacent 64-byte halves) instead of 32 STS.16
@@ -693,24 +638,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
                 *reinterpret_cast<uint32_t*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
                                              (lane & 6) * 2) = w;  // V^T is fp16 (PV runs in fp16)
               }
-#else
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const uint32_t dd = 32 * h + i;
-                *reinterpret_cast<__half*>(buf + dd * 64 + ((((lane >> 3) ^ ((dd >> 1) & 3))) * 16) +
-                                           (lane & 7) * 2) = __float2half_rn(v[i]);  // V^T is fp16 (PV runs in fp16)
-              }
-#endif
             }
           }
-          if (!SF_QKV_LD64 && c0 + 64 >= COLS) {
-            acc_release(acc);
-          }
           if (warp == 2 && lane == 0) GTR(6, 3 * local + c0 / 64);
-          if (which < 2 || SF_QKV_DIAG_NOVT)
-            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), do_store && r0 < ep.M);
+          if (which < 2)
+            out.release(lane, &maps.d[which < 2 ? which : 1], buf, 0, (int)(hb * T + tok0), r0 < ep.M);
           else
-            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), do_store && r0 < ep.M);
+            out.release(lane, &maps.d[2], buf, tok0, (int)(hb * 64), r0 < ep.M);
           if (warp == 2 && lane == 0) GTR(7, 3 * local + c0 / 64);
         }
       } else if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES_LN2) {
@@ -754,7 +688,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
         const float* vshift = vb + 2 * BN + c_lo;
         const float* vscale = vb + 3 * BN + c_lo;
         const uint32_t tcol = taddr + c_lo;
-        const bool st_ok = do_store && r0 < ep.M;
+        const bool st_ok = r0 < ep.M;
         // pass 1: x_new = x + gate*(acc + bias) -> bf16 residual (TMA store), kept in
         // registers as bf16 pairs (LayerNorm sees the stored, rounded residual);
         // partial row sum.  The accumulator is released right after its last TMEM

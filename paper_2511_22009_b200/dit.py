@@ -154,7 +154,7 @@ _lib.RESTYPES["sf_dit_launch_count"] = C.c_int64
 _lib.RESTYPES["sf_dit_graph_count"] = C.c_int64
 
 PROFILE_CLASSES = ("prepare", "cond", "adaln_gemm", "patch_embed_ln", "qkv_gemm", "attention",
-                   "proj_gemm_res_ln", "fc1_gemm_gelu", "fc2_gemm_res_ln", "final_euler_refill", "mlp_fused", "block_tail")
+                   "proj_gemm_res_ln", "fc1_gemm_gelu", "fc2_gemm_res_ln", "final_euler_refill", "block_tail")
 
 
 class DeviceDiT:

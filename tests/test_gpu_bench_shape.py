@@ -5,11 +5,11 @@ At these sizes the persistent kernels walk many 128-row tiles per CTA (block tai
 1024 tiles over 148 CTAs), so the cross-tile pipeline phases -- which a <=16-row test
 never reaches -- are what runs.  Checks:
 
-* block tail / fused MLP at M = 320 slots x 1024 tokens (17+ tiles per CTA): against
-  the torch-fp32 formula of the block (same tolerance as tests/test_gpu_dit_ops.py),
-  and BIT-EXACT against the same kernel run in 8-slot chunks (64 tiles -> one tile per
-  CTA): a 128-row tile's arithmetic must not depend on which CTA or pipeline phase
-  computed it;
+* block tail at M = 320 slots x 1024 tokens (2560 row tiles = 1280 CTA-pair tiles over 74
+  clusters: 17+ per pair): against the torch-fp32 formula of the block (same tolerance as
+  tests/test_gpu_dit_ops.py), and BIT-EXACT against the same kernel run in 8-slot chunks (32
+  pair tiles -> one per cluster): a 128-row tile's arithmetic must not depend on which CTA
+  pair or pipeline phase computed it;
 * DeviceDiT.forward at 128 / 256 rows: bit-identical to 8-row chunks (row independence,
   flowpipe models.py:92-96), first and last chunk against the fp32 oracle on the GPU;
 * the bench's own StreamBatch (S=32, device noise, CUDA graph) equal to eager launches
@@ -41,7 +41,7 @@ def bf(x):
     return x.to(torch.bfloat16)
 
 
-def _mlp_inputs(slots, seed):
+def _tail_inputs(slots, seed):
     g = torch.Generator(device="cuda").manual_seed(seed)
     M = slots * T
     d = {
@@ -68,13 +68,6 @@ def _tail(d, xres, xmod, r0, r1):
              p(v[:, 3 * N:]), p(v[:, 4 * N:]), p(v[:, 5 * N:]), vs, 1e-6, (r1 - r0) * T, T, st())
 
 
-def _mlp(d, xres, xmod, r0, r1):
-    p = lambda t: t.data_ptr()
-    v = d["vecs"][r0:]
-    L().call("sf_mlp_fused", p(xmod[r0 * T:]), p(d["w1"]), p(d["w2"]), p(d["b1"]), p(d["b2"]), p(xres[r0 * T:]),
-             p(xmod[r0 * T:]), p(v[:, 3 * N:]), p(v[:, 4 * N:]), p(v[:, 5 * N:]), 8 * N, 1e-6, (r1 - r0) * T, T, st())
-
-
 def _tail_ref(d, r0, r1):
     """torch fp32 block tail for slots [r0, r1) (bf16 rounding where the kernel stores bf16)."""
     sl = slice(r0 * T, r1 * T)
@@ -88,22 +81,13 @@ def _tail_ref(d, r0, r1):
     return x2, ln(x2) * (1 + sc2) + sh2
 
 
-def _mlp_ref(d, x, r0, r1):
-    sl = slice(r0 * T, r1 * T)
-    v = d["vecs"][r0:r1].repeat_interleave(T, 0)
-    g2, sh2, sc2 = (v[:, i * N:(i + 1) * N] for i in range(3, 6))
-    hh = torch.nn.functional.gelu(x[sl].float() @ d["w1"].float().t() + d["b1"], approximate="tanh")
-    y = d["xres0"][sl].float() + g2 * (hh.to(torch.bfloat16).float() @ d["w2"].float().t() + d["b2"])
-    return y, torch.nn.functional.layer_norm(y, (N,), eps=1e-6) * (1 + sc2) + sh2
-
-
-SLOTS = 320  # 2560 row tiles: >= 17 per persistent CTA on 148 SMs
-CHUNK = 8    # 64 tiles: one per CTA
+SLOTS = 320  # 2560 row tiles: >= 17 pair tiles per persistent cluster of 2 CTAs
+CHUNK = 8    # 64 tiles: one pair tile per cluster
 
 
 def test_block_tail_multi_tile_bench_shape():
     torch.backends.cuda.matmul.allow_tf32 = False
-    d = _mlp_inputs(SLOTS, 91)
+    d = _tail_inputs(SLOTS, 91)
     M = SLOTS * T
     xres, xmod = d["xres0"].clone(), torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     _tail(d, xres, xmod, 0, SLOTS)
@@ -120,26 +104,6 @@ def test_block_tail_multi_tile_bench_shape():
         assert (xres[sl].float() - x2).abs().max().item() < 3e-2 * max(1.0, x2.abs().max().item())
         assert (xmod[sl].float() - out).abs().max().item() < 5e-2 * max(1.0, out.abs().max().item())
     assert torch.isfinite(xmod.float()).all()
-
-
-def test_mlp_fused_multi_tile_bench_shape():
-    torch.backends.cuda.matmul.allow_tf32 = False
-    d = _mlp_inputs(SLOTS, 92)
-    M = SLOTS * T
-    x = d["attn"]  # any bf16 [M, N] input
-    xres, xmod = d["xres0"].clone(), x.clone()
-    _mlp(d, xres, xmod, 0, SLOTS)
-    xres_c, xmod_c = d["xres0"].clone(), x.clone()
-    for r0 in range(0, SLOTS, CHUNK):
-        _mlp(d, xres_c, xmod_c, r0, r0 + CHUNK)
-    torch.cuda.synchronize()
-    assert torch.equal(xres, xres_c) and torch.equal(xmod, xmod_c), "fused MLP: multi-tile CTAs differ"
-    for r0 in (0, 201, SLOTS - 4):
-        y, out = _mlp_ref(d, x, r0, r0 + 4)
-        sl = slice(r0 * T, (r0 + 4) * T)
-        assert (xres[sl].float() - y).abs().max().item() < 3e-2 * max(1.0, y.abs().max().item())
-        assert (xmod[sl].float() - out).abs().max().item() < 5e-2 * max(1.0, out.abs().max().item())
-    assert M == xres.shape[0]
 
 
 @pytest.fixture(scope="module")

@@ -1,6 +1,6 @@
 """DiT building blocks on sm_100a vs plain torch fp32 references of the same op:
 QKV GEMM with head-major scatter, gated-residual + LayerNorm + modulate
-epilogue, and tcgen05 flash attention."""
+epilogue, tcgen05 flash attention, and the fused block tail."""
 
 import math
 
@@ -108,52 +108,11 @@ def test_attention_hd72_matches_sdpa(rows, H, scale):
     assert err < 2e-2, err
 
 
-@pytest.mark.parametrize("rows", [1, 2, 3])
-def test_mlp_fused_matches_unfused(rows):
-    """sf_mlp_fused (fc1+GELU+fc2+gated residual+LN+modulate, hidden on chip) vs torch fp32
-    of the same block with the hidden rounded to bf16 (as the unfused path stores it), and
-    vs the unfused GEMM pair (sf_gemm_bf16 GELU -> sf_gemm_res_ln)."""
-    T, N, F = 1024, 384, 1536
-    M = rows * T
-    g = torch.Generator(device="cuda").manual_seed(40 + rows)
-    x = bf(torch.randn(M, N, device="cuda", generator=g))
-    w1 = bf(torch.randn(F, N, device="cuda", generator=g) * 0.05)
-    b1 = torch.randn(F, device="cuda", generator=g) * 0.1
-    w2 = bf(torch.randn(N, F, device="cuda", generator=g) * 0.03)
-    b2 = torch.randn(N, device="cuda", generator=g) * 0.1
-    xres0 = bf(torch.randn(M, N, device="cuda", generator=g))
-    vec_stride = 4 * N
-    vecs = torch.randn(rows, vec_stride, device="cuda", generator=g) * 0.5
-    gate, shift, scale = vecs[:, 0:N], vecs[:, N:2 * N], vecs[:, 2 * N:3 * N]
-    # fused (xmod in place, as the runtime uses it)
-    xres = xres0.clone()
-    xmod = x.clone()
-    L().call("sf_mlp_fused", xmod.data_ptr(), w1.data_ptr(), w2.data_ptr(), b1.data_ptr(), b2.data_ptr(),
-             xres.data_ptr(), xmod.data_ptr(), gate.data_ptr(), shift.data_ptr(), scale.data_ptr(), vec_stride,
-             1e-6, M, T, st())
-    # unfused pair
-    h = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
-    L().call("sf_gemm_bf16", x.data_ptr(), w1.data_ptr(), b1.data_ptr(), h.data_ptr(), M, F, N, 2, st())
-    xres_u = xres0.clone()
-    xmod_u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    L().call("sf_gemm_res_ln", h.data_ptr(), w2.data_ptr(), b2.data_ptr(), xres_u.data_ptr(), xmod_u.data_ptr(),
-             gate.data_ptr(), shift.data_ptr(), scale.data_ptr(), vec_stride, M, N, F, T, 1e-6, st())
-    torch.cuda.synchronize()
-    slot = torch.arange(M, device="cuda") // T
-    hh = torch.nn.functional.gelu(x.float() @ w1.float().t() + b1, approximate="tanh").to(torch.bfloat16).float()
-    y = xres0.float() + gate[slot] * (hh @ w2.float().t() + b2)
-    ref = torch.nn.functional.layer_norm(y, (N,), eps=1e-6) * (1 + scale[slot]) + shift[slot]
-    for got_r, got_m in ((xres, xmod), (xres_u, xmod_u)):
-        assert (got_r.float() - y).abs().max().item() < 3e-2 * max(1.0, y.abs().max().item())
-        assert (got_m.float() - ref).abs().max().item() < 5e-2 * max(1.0, ref.abs().max().item())
-    # fused and unfused agree to bf16 rounding of the same hidden
-    assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, y.abs().max().item())
-
-
-@pytest.mark.parametrize("rows", [1, 2])
-def test_block_tail_matches_proj_plus_mlp(rows):
-    """sf_block_tail (projection + residual + LN + fused MLP + residual + LN in one kernel) vs
-    the two-kernel path sf_gemm_res_ln (projection) -> sf_mlp_fused, and vs torch fp32."""
+@pytest.mark.parametrize("rows", [2, 4])
+def test_block_tail_matches_gemm_path(rows):
+    """sf_block_tail (projection + residual + LN + MLP + residual + LN in one kernel on CTA pairs)
+    vs the GEMM path sf_gemm_res_ln (projection) -> sf_gemm_bf16 GELU (fc1) -> sf_gemm_res_ln
+    (fc2), and vs torch fp32."""
     T, N, F = 1024, 384, 1536
     M = rows * T
     g = torch.Generator(device="cuda").manual_seed(70 + rows)
@@ -175,13 +134,16 @@ def test_block_tail_matches_proj_plus_mlp(rows):
     xmod = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     L().call("sf_block_tail", ptr(attn), ptr(wp), ptr(bp), ptr(w1), ptr(w2), ptr(b1), ptr(b2), ptr(xres), ptr(xmod),
              ptr(g1), ptr(sh1), ptr(sc1), ptr(g2), ptr(sh2), ptr(sc2), vs, 1e-6, M, T, st())
-    # two kernels
+    # three GEMMs
     xres_u = xres0.clone()
+    h_u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    hid = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
     xmod_u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    L().call("sf_gemm_res_ln", ptr(attn), ptr(wp), ptr(bp), ptr(xres_u), ptr(xmod_u), ptr(g1), ptr(sh1), ptr(sc1),
+    L().call("sf_gemm_res_ln", ptr(attn), ptr(wp), ptr(bp), ptr(xres_u), ptr(h_u), ptr(g1), ptr(sh1), ptr(sc1),
              vs, M, N, N, T, 1e-6, st())
-    L().call("sf_mlp_fused", ptr(xmod_u), ptr(w1), ptr(w2), ptr(b1), ptr(b2), ptr(xres_u), ptr(xmod_u), ptr(g2),
-             ptr(sh2), ptr(sc2), vs, 1e-6, M, T, st())
+    L().call("sf_gemm_bf16", ptr(h_u), ptr(w1), ptr(b1), ptr(hid), M, F, N, 2, st())
+    L().call("sf_gemm_res_ln", ptr(hid), ptr(w2), ptr(b2), ptr(xres_u), ptr(xmod_u), ptr(g2), ptr(sh2), ptr(sc2),
+             vs, M, N, F, T, 1e-6, st())
     torch.cuda.synchronize()
     slot = torch.arange(M, device="cuda") // T
     ln = lambda x: torch.nn.functional.layer_norm(x, (N,), eps=1e-6)
@@ -196,9 +158,9 @@ def test_block_tail_matches_proj_plus_mlp(rows):
     assert (xres.float() - xres_u.float()).abs().max().item() < 2e-2 * max(1.0, x2.abs().max().item())
 
 
-def test_fused_kernels_reject_bad_shapes():
-    """The fused MLP / block-tail entry points refuse row counts that are not whole
-    128-row tiles of whole slots (ParameterError, like the reference's shape checks)."""
+def test_block_tail_rejects_bad_shapes():
+    """sf_block_tail refuses row counts that are not whole pairs of 128-row tiles of whole slots,
+    and null pointers (ParameterError, like the reference's shape checks)."""
     from paper_2511_22009_b200.errors import ParameterError
 
     N, F = 384, 1536
@@ -207,12 +169,11 @@ def test_fused_kernels_reject_bad_shapes():
     w2 = torch.zeros(N, F, device="cuda", dtype=torch.bfloat16)
     b = torch.zeros(F, device="cuda")
     v = torch.zeros(1, 8 * N, device="cuda")
-    with pytest.raises(ParameterError):  # M not a multiple of 128
-        L().call("sf_mlp_fused", z.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(), b.data_ptr(), z.data_ptr(),
-                 z.data_ptr(), v.data_ptr(), v.data_ptr(), v.data_ptr(), 8 * N, 1e-6, 200, 200, st())
+    args = lambda a0, M, T: (a0, z.data_ptr(), b.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(), b.data_ptr(),
+                             z.data_ptr(), z.data_ptr(), *([v.data_ptr()] * 6), 8 * N, 1e-6, M, T, st())
+    with pytest.raises(ParameterError):  # M not a multiple of 256 (one 128-row tile)
+        L().call("sf_block_tail", *args(z.data_ptr(), 128, 128))
     with pytest.raises(ParameterError):  # tokens per slot not a multiple of 128
-        L().call("sf_block_tail", *([z.data_ptr()] * 2), b.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(),
-                 b.data_ptr(), z.data_ptr(), z.data_ptr(), *([v.data_ptr()] * 6), 8 * N, 1e-6, 256, 100, st())
+        L().call("sf_block_tail", *args(z.data_ptr(), 256, 100))
     with pytest.raises(ParameterError):  # null pointer
-        L().call("sf_block_tail", None, z.data_ptr(), b.data_ptr(), w1.data_ptr(), w2.data_ptr(), b.data_ptr(),
-                 b.data_ptr(), z.data_ptr(), z.data_ptr(), *([v.data_ptr()] * 6), 8 * N, 1e-6, 256, 128, st())
+        L().call("sf_block_tail", *args(None, 256, 128))

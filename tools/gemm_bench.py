@@ -10,9 +10,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_22009_b200 import _lib  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 131072
-if "--2sm" in sys.argv:  # cta_group::2 pair tiles for fc1 / QKV (off by default)
-    import ctypes
-    ctypes.CDLL(_lib.LIB_PATH).sf_diag_gemm_2sm(1)
 T, H, D = 1024, 6, 384
 st = torch.cuda.current_stream().cuda_stream
 bf = lambda t: t.to(torch.bfloat16)
@@ -67,25 +64,13 @@ for flag, name in ((0x102, "fc1 gelu nostore"), (0x101, "fc1 bf16 nostore"), (0x
     ms = timeit(lambda: _lib.call("sf_gemm_bf16", a.data_ptr(), w1.data_ptr(), b1.data_ptr(), o1.data_ptr(), M, 4 * D,
                                   D, flag, st))
     print(f"{name:18s}: {ms*1e3:7.1f} us {2*M*4*D*D/ms/1e9:7.1f} TFLOP/s")
-for n in (256, 512, 1024, 2048):
-    wq = bf(torch.randn(n, D, device=dev) * 0.05)
-    bq = torch.zeros(n, device=dev)
-    oq = torch.empty(M, n, device=dev, dtype=torch.bfloat16)
-    ms = timeit(lambda: _lib.call("sf_gemm_bf16", a.data_ptr(), wq.data_ptr(), bq.data_ptr(), oq.data_ptr(), M, n, D,
-                                  0x201, st))
-    print(f"mainloop only N={n} K={D}: {ms*1e3:7.1f} us {2*M*n*D/ms/1e9:7.1f} TFLOP/s")
-import ctypes
-lib = ctypes.CDLL(_lib.LIB_PATH)
-for mode in (3, 4):
-    lib.sf_diag_res_ln(mode)
-    for name, A, K in (("proj", a, D), ("fc2", h, 4 * D)):
-        w2 = bf(torch.randn(D, K, device=dev) * 0.05)
-        b2 = torch.zeros(D, device=dev)
-        xres = bf(torch.randn(M, D, device=dev))
-        xmod = torch.empty(M, D, device=dev, dtype=torch.bfloat16)
-        vec = torch.randn(rows, 3 * D, device=dev) * 0.1
-        ms = timeit(lambda: _lib.call("sf_gemm_res_ln", A.data_ptr(), w2.data_ptr(), b2.data_ptr(), xres.data_ptr(),
-                                      xmod.data_ptr(), vec.data_ptr(), vec[:, D:].data_ptr(), vec[:, 2 * D:].data_ptr(),
-                                      3 * D, M, D, K, T, 1e-6, st))
-        print(f"{name:5s} diag={mode} N={D} K={K}: {ms*1e3:7.1f} us {2*M*D*K/ms/1e9:7.1f} TFLOP/s")
-lib.sf_diag_res_ln(0)
+for name, A, K in (("proj", a, D), ("fc2", h, 4 * D)):
+    w2 = bf(torch.randn(D, K, device=dev) * 0.05)
+    b2 = torch.zeros(D, device=dev)
+    xres = bf(torch.randn(M, D, device=dev))
+    xmod = torch.empty(M, D, device=dev, dtype=torch.bfloat16)
+    vec = torch.randn(rows, 3 * D, device=dev) * 0.1
+    ms = timeit(lambda: _lib.call("sf_gemm_res_ln", A.data_ptr(), w2.data_ptr(), b2.data_ptr(), xres.data_ptr(),
+                                  xmod.data_ptr(), vec.data_ptr(), vec[:, D:].data_ptr(), vec[:, 2 * D:].data_ptr(),
+                                  3 * D, M, D, K, T, 1e-6, st))
+    print(f"{name:5s} res+LN N={D} K={K}: {ms*1e3:7.1f} us {2*M*D*K/ms/1e9:7.1f} TFLOP/s")

@@ -8,8 +8,6 @@ from paper_2511_22009_b200 import _lib
 which = sys.argv[1] if len(sys.argv) > 1 else "fc1"
 M, D, T, H = 131072, 384, 1024, 6
 st = torch.cuda.current_stream().cuda_stream
-if "--2sm" in sys.argv:
-    ctypes.CDLL(_lib.LIB_PATH).sf_diag_gemm_2sm(1)
 bf = lambda t: t.to(torch.bfloat16)
 a = bf(torch.randn(M, D, device="cuda"))
 h = bf(torch.randn(M, 4 * D, device="cuda"))
