@@ -139,11 +139,13 @@ int sf_stream_prepare(int64_t* ctl, int64_t S, int32_t n, int64_t m, const doubl
  *   (-1 when nothing retired this iteration), noise_in [S, D] fp64: initial
  *   noise of generation j+1 per stream (pipeline.py:92-98), ignored when
  *   j+1 >= m.  emb / neg: [S, E] fp64 (neg may be NULL = zeros,
- *   models.py:258-260).  model_seed: SeededMockModel seed. */
+ *   models.py:258-260).  model_seed: SeededMockModel seed.  w_streams: NULL (every
+ *   stream uses w) or device fp64 [S] per-stream guidance scales (a stream with
+ *   w_s == 1 runs unguided, exactly as its own run_stream would). */
 int sf_stream_mock_step(const int64_t* ctl, int64_t S, int32_t n, int64_t m, int64_t D, int x_dtype, void* x_ring,
                         const double* stage_params, const int64_t* row_info, const double* row_t, int64_t model_seed,
-                        const double* emb, const double* neg, int32_t E, double w, const double* noise_in,
-                        void* frames_out, int64_t* frame_ids, void* stream);
+                        const double* emb, const double* neg, int32_t E, double w, const double* w_streams,
+                        const double* noise_in, void* frames_out, int64_t* frame_ids, void* stream);
 
 /* Write generation-0 noise into slot 0 of every stream and reset ctl (j = 0). */
 int sf_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, int x_dtype, void* x_ring,
@@ -254,7 +256,8 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
 
 /* One stream-batch iteration with the DiT (pipeline.py:171-219) fully on device:
  * ring bookkeeping, one guided velocity evaluation over all S*n slots (2x rows
- * when w != 1, models.py:244-296), fused CFG + Euler + emit + refill on the
+ * when w != 1, models.py:244-296; w_streams = NULL or device fp64 [S] per-stream
+ * scales, w != 1 then only says "some stream is guided"), fused CFG + Euler + emit + refill on the
  * fp32 ring x_ring [S*n, D].  noise_in [S, D] fp32 = initial noise of
  * generation j+1 per stream, or NULL for on-device Philox(noise_seed + s).
  * use_graph != 0 captures the launch sequence into a CUDA graph on first use
@@ -263,8 +266,8 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
  * eager launch sequence for the same arguments. */
 int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
-                       const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
-                       int32_t use_graph, void* stream);
+                       const double* w_streams, const float* noise_in, uint64_t noise_seed, float* frames_out,
+                       int64_t* frame_ids, int32_t use_graph, void* stream);
 
 /* One eager (non-graph) stream step with a CUDA event after every launch;
  * synchronises and returns, per kernel class, the summed duration (ms) and the
@@ -273,8 +276,9 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
  * 8 fc2 GEMM+res+LN, 9 final+CFG+Euler+refill (arrays of >= 10 entries). */
 int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                         int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
-                        double w, const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
-                        float* ms_per_class, int32_t* launches_per_class, void* stream);
+                        double w, const double* w_streams, const float* noise_in, uint64_t noise_seed,
+                        float* frames_out, int64_t* frame_ids, float* ms_per_class, int32_t* launches_per_class,
+                        void* stream);
 
 /* Number of kernel launches this handle has issued or captured so far. */
 int64_t sf_dit_launch_count(const sf_dit* h);

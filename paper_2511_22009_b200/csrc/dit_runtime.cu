@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
     int P, int C, int64_t lat_rows, float* __restrict__ eps_out, const int64_t* __restrict__ ctl, int n, int64_t m,
     const double* __restrict__ stage_params, const int64_t* __restrict__ row_info, int cfg, float w,
-    float* __restrict__ x_ring, const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
+    const double* __restrict__ w_streams, float* __restrict__ x_ring, const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
     int64_t* __restrict__ frame_ids, int64_t total_tokens) {
   constexpr int PK = 16;
   constexpr int WROW = HID * 2 + FINAL_WPAD;  // bytes
@@ -555,14 +555,17 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     float e[2][4];
     project(STREAM && cfg ? lr + lat_rows : lr, tau0, e);
     if constexpr (STREAM) {
-      if (cfg) {
+      // per-stream guidance: a stream with w == 1 takes the conditional eps as is (apply_cfg is
+      // the identity for it, models.py:254-255; row independence makes its cond row exact)
+      const float wl = w_streams ? (float)w_streams[row_info[lr * 4 + 3]] : w;
+      if (cfg && wl != 1.0f) {
         float eu[2][4];
         project(lr, tau0, eu);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
           for (int i = 0; i < 4; ++i)  // handle_cfg (models.py:288-293)
-            e[nt][i] = __fadd_rn(eu[nt][i], __fmul_rn(w, __fsub_rn(e[nt][i], eu[nt][i])));
+            e[nt][i] = __fadd_rn(eu[nt][i], __fmul_rn(wl, __fsub_rn(e[nt][i], eu[nt][i])));
       }
     }
 #pragma unroll
@@ -614,7 +617,8 @@ struct sf_dit {
   // sequence an eager call with the same arguments would enqueue.  Owners release their graphs
   // (sf_dit_graph_release) when their buffers are freed; the cache is also capped.
   using GraphKey = std::tuple<const void*, int64_t, int, int64_t, const void*, const void*, const void*, const void*,
-                              const void*, const void*, double, const void*, uint64_t, const void*, const void*>;
+                              const void*, const void*, double, const void*, const void*, uint64_t, const void*,
+                              const void*>;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
   // profiling / accounting
@@ -786,7 +790,8 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
 // Final layer + Euler/emit/refill (mma.sync kernel).
 template <bool STREAM>
 static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int64_t* ctl, int n, int64_t m,
-                         const double* stage_params, const int64_t* row_info, int cfg, float w, float* x_ring,
+                         const double* stage_params, const int64_t* row_info, int cfg, float w,
+                         const double* w_streams, float* x_ring,
                          const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
                          int64_t tokens, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
@@ -796,7 +801,8 @@ static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int6
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + 7) / 8, 148 * 8);
   auto fk = c.hidden == 384 ? final_layer_mma_kernel<384, STREAM> : final_layer_mma_kernel<1152, STREAM>;
   fk<<<blocks, 256, sm, st>>>(h->xmod, fw, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
-                              stage_params, row_info, cfg, w, x_ring, noise_in, noise_seed, frames_out, frame_ids,
+                              stage_params, row_info, cfg, w, w_streams, x_ring, noise_in, noise_seed, frames_out,
+                              frame_ids,
                               tokens);
 }
 
@@ -900,15 +906,15 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if ((rc = launch_patch(h, x, rows, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = rows * h->tokens;
-  launch_final<false>(h, rows, eps_out, nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, 0, nullptr, nullptr,
-                      tokens, st);
+  launch_final<false>(h, rows, eps_out, nullptr, 1, 1, nullptr, nullptr, 0, 1.0f, nullptr, nullptr, nullptr, 0, nullptr,
+                      nullptr, tokens, st);
   return cuda_status();
 }
 
 static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                                 int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
-                                double w, const float* noise_in, uint64_t noise_seed, float* frames_out,
-                                int64_t* frame_ids, cudaStream_t st) {
+                                double w, const double* w_streams, const float* noise_in, uint64_t noise_seed,
+                                float* frames_out, int64_t* frame_ids, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const int64_t R = S * n;
   const int cfg = (w != 1.0) ? 1 : 0;
@@ -922,15 +928,16 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;
   if ((rc = run_blocks(h, rows, st))) return rc;
   const int64_t tokens = R * h->tokens;
-  launch_final<true>(h, R, nullptr, ctl, n, m, stage_params, row_info, cfg, (float)w, x_ring, noise_in, noise_seed,
-                     frames_out, frame_ids, tokens, st);
+  launch_final<true>(h, R, nullptr, ctl, n, m, stage_params, row_info, cfg, (float)w, w_streams, x_ring, noise_in,
+                     noise_seed, frames_out, frame_ids, tokens, st);
   mark(h, P_FINAL, st);
   return cuda_status();
 }
 
 int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                         int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg,
-                        double w, const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                        double w, const double* w_streams, const float* noise_in, uint64_t noise_seed,
+                        float* frames_out, int64_t* frame_ids,
                         float* ms_per_class, int32_t* launches_per_class, void* stream) {
   if (!h || S < 1 || n < 1 || m < 1 || !ms_per_class || !launches_per_class) return SF_ERR_PARAMETER;
   const int64_t rows = (w != 1.0 ? 2 : 1) * S * n;
@@ -942,7 +949,7 @@ int sf_dit_profile_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m
   cudaEvent_t start;
   cudaEventCreate(&start);
   cudaEventRecord(start, st);
-  int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+  int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, w_streams, noise_in,
                                 noise_seed, frames_out, frame_ids, st);
   h->profiling = false;
   if (cudaStreamSynchronize(st) != cudaSuccess) rc = SF_ERR_CUDA;
@@ -969,18 +976,19 @@ int64_t sf_dit_launch_count(const sf_dit* h) { return h ? h->launch_count : -1; 
 
 int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m, const double* stage_params,
                        int64_t* row_info, double* row_t, float* x_ring, const double* emb, const double* neg, double w,
-                       const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
+                       const double* w_streams, const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
                        int32_t use_graph, void* stream) {
   if (!h || S < 1 || n < 1 || m < 1) return SF_ERR_PARAMETER;
   const int64_t rows = (w != 1.0 ? 2 : 1) * S * n;
   if (rows > h->max_rows) return SF_ERR_PARAMETER;
   cudaStream_t st = (cudaStream_t)stream;
   if (!use_graph)
-    return stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+    return stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, w_streams, noise_in,
                                 noise_seed, frames_out, frame_ids, st);
   const sf_dit::GraphKey key{(const void*)ctl, S,          n, m, (const void*)stage_params, (const void*)row_info,
                              (const void*)row_t, (const void*)x_ring, (const void*)emb, (const void*)neg, w,
-                             (const void*)noise_in, noise_seed, (const void*)frames_out, (const void*)frame_ids};
+                             (const void*)w_streams, (const void*)noise_in, noise_seed, (const void*)frames_out,
+                             (const void*)frame_ids};
   auto it = h->graphs.find(key);
   if (it == h->graphs.end()) {
     if (h->graphs.size() >= kMaxGraphs) {  // cap: drop every cached graph (re-captured on next use)
@@ -994,7 +1002,7 @@ int sf_dit_stream_step(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, int64_t m,
       return SF_ERR_CUDA;
     cudaGraph_t g;
     if (cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return SF_ERR_CUDA;
-    int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, noise_in,
+    int rc = stream_step_launches(h, ctl, S, n, m, stage_params, row_info, row_t, x_ring, emb, neg, w, w_streams, noise_in,
                                   noise_seed, frames_out, frame_ids, h->cap_stream);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     if (rc != SF_OK || e != cudaSuccess) return rc != SF_OK ? rc : SF_ERR_CUDA;

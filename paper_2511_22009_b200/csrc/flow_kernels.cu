@@ -286,8 +286,8 @@ template <typename TX>
 __global__ void stream_mock_step_kernel(const int64_t* ctl, int64_t S, int n, int64_t m, int64_t D, TX* x_ring,
                                         const double* __restrict__ stage_params, const int64_t* __restrict__ row_info,
                                         const double* __restrict__ row_t, int64_t seed, const double* emb,
-                                        const double* neg, int E, double w, const double* __restrict__ noise_in,
-                                        TX* frames_out, int64_t* frame_ids) {
+                                        const double* neg, int E, double w, const double* __restrict__ w_streams,
+                                        const double* __restrict__ noise_in, TX* frames_out, int64_t* frame_ids) {
   __shared__ uint64_t s_keys[2];
   const int64_t r = blockIdx.y;
   const int64_t j = ctl[1];
@@ -299,7 +299,8 @@ __global__ void stream_mock_step_kernel(const int64_t* ctl, int64_t S, int n, in
   const bool refill_slot = (k == (j + 1) % n);
   const bool admit = refill_slot && (j + 1 < m);
   const bool retiring = active && (stage + 1 == n);
-  const bool guided = (w != 1.0);  // pipeline.py:113
+  const double ws = w_streams ? w_streams[s] : w;  // this stream's guidance scale
+  const bool guided = (ws != 1.0);                 // pipeline.py:113
   if (active && threadIdx.x == 0) {
     const double t = row_t[r];
     // apply_cfg (models.py:257-268): uncond half uses the negative embedding (zeros when absent)
@@ -321,7 +322,7 @@ __global__ void stream_mock_step_kernel(const int64_t* ctl, int64_t S, int n, in
       double e = splitmix_unit(s_keys[1], (uint64_t)i);
       if (guided) {  // handle_cfg (models.py:288-293), fp64 like the mock's output
         const double eu = splitmix_unit(s_keys[0], (uint64_t)i);
-        e = __dadd_rn(eu, __dmul_rn(w, __dsub_rn(e, eu)));
+        e = __dadd_rn(eu, __dmul_rn(ws, __dsub_rn(e, eu)));
       }
       const TX xn = euler(xr[i], cast_to<TX>(e), c);
       if (retiring) frames_out[s * D + i] = xn;
@@ -468,19 +469,19 @@ int sf_stream_prepare(int64_t* ctl, int64_t S, int32_t n, int64_t m, const doubl
 
 int sf_stream_mock_step(const int64_t* ctl, int64_t S, int32_t n, int64_t m, int64_t D, int x_dtype, void* x_ring,
                         const double* stage_params, const int64_t* row_info, const double* row_t, int64_t model_seed,
-                        const double* emb, const double* neg, int32_t E, double w, const double* noise_in,
-                        void* frames_out, int64_t* frame_ids, void* stream) {
+                        const double* emb, const double* neg, int32_t E, double w, const double* w_streams,
+                        const double* noise_in, void* frames_out, int64_t* frame_ids, void* stream) {
   if (S < 1 || n < 1 || m < 1 || D < 1 || E < 1 || E > 64 || S * n > 65535) return SF_ERR_PARAMETER;
   dim3 grid(grid_for(D, 256) > 16 ? 16 : grid_for(D, 256), (unsigned)(S * n));
   cudaStream_t st = (cudaStream_t)stream;
   if (x_dtype == SF_F64)
     stream_mock_step_kernel<double><<<grid, 256, 0, st>>>(ctl, S, n, m, D, (double*)x_ring, stage_params, row_info,
-                                                          row_t, model_seed, emb, neg, E, w, noise_in,
-                                                          (double*)frames_out, frame_ids);
+                                                          row_t, model_seed, emb, neg, E, w, w_streams,
+                                                          noise_in, (double*)frames_out, frame_ids);
   else if (x_dtype == SF_F32)
     stream_mock_step_kernel<float><<<grid, 256, 0, st>>>(ctl, S, n, m, D, (float*)x_ring, stage_params, row_info,
-                                                         row_t, model_seed, emb, neg, E, w, noise_in,
-                                                         (float*)frames_out, frame_ids);
+                                                         row_t, model_seed, emb, neg, E, w, w_streams,
+                                                         noise_in, (float*)frames_out, frame_ids);
   else
     return SF_ERR_PARAMETER;
   return cuda_status();

@@ -139,12 +139,12 @@ _lib.SIGNATURES.update({
     "sf_dit_destroy": [C.c_void_p],
     "sf_dit_forward": [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "sf_dit_stream_step": [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
-                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
                            C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p],
     "sf_dit_stream_reset": [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                             C.c_uint64, C.c_void_p],
     "sf_dit_profile_step": [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
-                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
                             C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     "sf_dit_launch_count": [C.c_void_p],
     "sf_dit_graph_release": [C.c_void_p, C.c_void_p],

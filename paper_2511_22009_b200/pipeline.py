@@ -16,6 +16,7 @@ j+1.  Everything between ``step()`` calls stays on the GPU.
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -182,10 +183,13 @@ class StreamBatch:
         conds = cond if isinstance(cond, (list, tuple)) else [cond] * self.S
         if len(conds) != self.S or any(c is None for c in conds):
             raise ParameterError("need one Conditioning (or a list of num_streams)")
-        ws = {c.guidance_scale for c in conds}
-        if len(ws) != 1:
-            raise ParameterError("all streams of one StreamBatch share the guidance scale")
-        self.w = float(ws.pop())
+        # guidance per stream (independent run_stream calls may differ): the batch is doubled when any
+        # stream is guided; the fused kernels combine with each stream's own w (w == 1: unguided)
+        scales = [float(c.guidance_scale) for c in conds]
+        guided = [w for w in scales if w != 1.0]
+        self.w = guided[0] if guided else 1.0
+        self.w_streams = (torch.tensor(scales, dtype=torch.float64, device=device)
+                          if len(set(scales)) > 1 else None)
         self.conds = conds
         self.seeds = list(seed) if isinstance(seed, (list, tuple)) else [int(seed) + s for s in range(self.S)]
         E = model.embed_dim
@@ -243,6 +247,9 @@ class StreamBatch:
             except Exception:
                 pass
 
+    def _wptr(self):
+        return None if self.w_streams is None else self.w_streams.data_ptr()
+
     # ------------------------------------------------------------------ admission noise
     def _fill_noise(self, gen: int) -> bool:
         """Stage generation `gen`'s initial noise for every stream; False if none."""
@@ -299,8 +306,8 @@ class StreamBatch:
             _lib.call("sf_dit_stream_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, n, m,
                       self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
                       self.x_ring.data_ptr(), self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
-                      self.w, self.noise_dev.data_ptr() if self.noise != "device" else None, self.noise_seed,
-                      self.frames.data_ptr(), self.frame_ids.data_ptr(), 1 if self.use_graph else 0, st)
+                      self.w, self._wptr(), self.noise_dev.data_ptr() if self.noise != "device" else None,
+                      self.noise_seed, self.frames.data_ptr(), self.frame_ids.data_ptr(), 1 if self.use_graph else 0, st)
         else:
             if self.noise == "device" and admit_next:
                 tmp = torch.empty(self.S, self.D, dtype=torch.float32, device=self.device)
@@ -313,8 +320,8 @@ class StreamBatch:
                           _lib.SF_F64 if self.t_dtype == torch.float64 else _lib.SF_F32, self.x_ring.data_ptr(),
                           self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
                           self.model.seed, self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
-                          self.model.embed_dim, self.w, self.noise_dev.data_ptr(), self.frames.data_ptr(),
-                          self.frame_ids.data_ptr(), st)
+                          self.model.embed_dim, self.w, self._wptr(), self.noise_dev.data_ptr(),
+                          self.frames.data_ptr(), self.frame_ids.data_ptr(), st)
             else:
                 self._generic_step(j)
         lo, hi = max(0, j - n + 1), min(j, m - 1)
@@ -399,8 +406,8 @@ class StreamBatch:
         _lib.call("sf_dit_profile_step", self.model.device_model.handle, self.ctl.data_ptr(), self.S, self.n, self.m,
                   self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
                   self.x_ring.data_ptr(), self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
-                  self.w, self.noise_dev.data_ptr() if self.noise != "device" else None, self.noise_seed,
-                  self.frames.data_ptr(), self.frame_ids.data_ptr(), ms, cnt, self._stream())
+                  self.w, self._wptr(), self.noise_dev.data_ptr() if self.noise != "device" else None,
+                  self.noise_seed, self.frames.data_ptr(), self.frame_ids.data_ptr(), ms, cnt, self._stream())
         self.j = j + 1
         return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PROFILE_CLASSES)}
 
@@ -461,7 +468,10 @@ def run_stream(m: int, n: int, model: VelocityModel, cond: Conditioning, seed: i
     extension: vae.TinyDecoder) decodes each retired frame on the device."""
     _check_run_args(m, n, sched)
     if isinstance(model, DiTVelocityModel) and np.dtype(dtype) == np.float64:
-        dtype = np.float32  # the DiT ring is fp32 (documented in DESIGN.md)
+        # the reference's default latent dtype is fp64; the DiT ring is fp32 (bf16 network): say so
+        warnings.warn("run_stream: the DiT velocity field keeps fp32 latents; dtype=float64 runs as float32",
+                      RuntimeWarning, stacklevel=2)
+        dtype = np.float32
     sb = StreamBatch(model, sched, n, num_streams=1, cond=cond, seed=seed, m=m, dtype=dtype, noise="numpy",
                      decoder=decoder)
     results = []

@@ -144,3 +144,25 @@ def test_window_params_and_mock_model_dropin(sf, golden):
     d2, c2 = sf.apply_cfg(batch, cond)
     out = sf.handle_cfg(model.forward(d2, c2), 7.5)
     assert np.array_equal(out.epsilon, golden["mock_eps_cfg"])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_mixed_guidance_scales_match_independent_runs(sf, dtype):
+    """Streams with different guidance scales (1.0 = unguided, as independent run_stream calls may
+    have) in ONE device batch == independent reference runs, bit for bit (per-stream w in the
+    fused step; a w == 1 stream takes its conditional eps unchanged)."""
+    S, m, n, k, D = 4, 5, 3, 4, 128
+    ws = [1.0, 7.5, 2.0, 1.0]
+    sched = sf.build_time_window_schedule(num_windows=k, inference_steps=n)
+    model = sf.SeededMockModel(dim=D, seed=4)
+    rng = np.random.default_rng(9)
+    embs = [rng.standard_normal(8) for _ in range(S)]
+    conds = [sf.make_conditioning(embs[s], guidance_scale=ws[s]) for s in range(S)]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=300, m=m, dtype=dtype)
+    out = sb()
+    osch = O.make_schedule(num_windows=k, steps=n)
+    for s in range(S):
+        fn = lambda ids, ts, x, s=s: O.guided_mock_eps(4, ids, ts, embs[s], None, ws[s], D)  # noqa: E731
+        run = O.run_stream(m, n, fn, 300 + s, osch, D, dtype=dtype)
+        for r in out[s]:
+            assert np.array_equal(r.latent, run.latents[r.id]), (s, r.id)
