@@ -39,8 +39,9 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   const int bn = hd == 64 ? qkv_bn64() : 144;
   const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
   if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
+  const int ctas = hd == 64 ? qkv_ctas(K) : 1;
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn, ctas) != SF_OK) return SF_ERR_CUDA;
   if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
@@ -48,7 +49,7 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   ep.q_scale = q_scale;
   ep.tokens_per_slot = T;
   ep.M = (int)M;
-  return launch_gemm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(EPI_QKV, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream, ctas);
 }
 
 int sf_gemm_qkv(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M, int32_t heads,

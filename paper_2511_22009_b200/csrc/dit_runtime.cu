@@ -703,7 +703,9 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.q_scale = 1.0f / sqrtf((float)hd);
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_QKV, hd == 64 ? qkv_bn64() : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_QKV, hd == 64 ? qkv_bn64() : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st,
+                            hd == 64 ? qkv_ctas(H) : 1)))
+        return rc;
       mark(h, P_QKV, st);
     }
     if ((rc = launch_attn(h->attn_maps, h->attn, rows, c.heads, T, st))) return rc;
@@ -857,7 +859,8 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     const __nv_bfloat16* fc1 = (const __nv_bfloat16*)w->fc1_w + (int64_t)l * c.mlp_hidden * H;
     const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
     const int hd = H / c.heads;
-    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? qkv_bn64() : 144);
+    rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? qkv_bn64() : 144,
+                            hd == 64 ? qkv_ctas(H) : 1);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
     if (H != 384) {  // DiT-XL/2 MLP + projection as GEMMs: RES epilogue (128-wide tiles) + LayerNorm pass
       rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);

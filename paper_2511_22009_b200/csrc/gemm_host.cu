@@ -48,10 +48,10 @@ int gemm_b_box_rows(int bn) { return bn > 256 ? bn / 2 : bn; }
 
 // 2-SM pair tiles: each CTA loads BN/2 rows of W per stage.
 
-int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn) {
+int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn, int ctas) {
   const int bk = gemm_bk(bn);
   int rc = make_tmap_bf16_2d(&m->a, A, K, M, K, bk, 128, 2 * bk);
-  rc |= make_tmap_bf16_2d(&m->b, W, K, N, K, bk, gemm_b_box_rows(bn), 2 * bk);
+  rc |= make_tmap_bf16_2d(&m->b, W, K, N, K, bk, gemm_b_box_rows(bn) / ctas, 2 * bk);
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
@@ -87,13 +87,17 @@ int make_qkv_out_maps(GemmMaps* m, const void* q, const void* k, const void* vt,
   return rc == SF_OK ? SF_OK : SF_ERR_CUDA;
 }
 
-// QKV tile width for head dim 64: 192 columns (3 heads per tile, 4 epilogue warps).
+// QKV tile width for head dim 64: 192 columns (3 heads per tile, 4 epilogue warps); with
+// K = 384 the tiles run on CTA pairs (256 x 192, B resident: gemm_tcgen05.cuh GemmCfg::B_RES).
 int qkv_bn64() { return 192; }
+int qkv_ctas(int64_t K) { return K == 64 * GemmCfg<192, 8, EPI_QKV, 2>::KB_RES ? 2 : 1; }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int CTAS = 1>
 constexpr int epi_warps() {
-  // QKV: 4; RES_LN: 12; bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
-  return KIND == EPI_QKV ? (BN == 192 ? 4 : BN == 128 ? 8 : 4) : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+  // QKV: 4 (pair tiles: 8 = two groups of 4 draining alternate tiles); RES_LN: 12;
+  // bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
+  return KIND == EPI_QKV ? (BN == 192 ? (CTAS == 2 ? 8 : 4) : BN == 128 ? 8 : 4)
+                         : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
 }
 
 // Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).
@@ -101,15 +105,16 @@ int gemm_narrow_out(int bn, int kind) {
   return (kind == EPI_RES_LN || kind == EPI_RES_LN2 || ((kind == EPI_BF16 || kind == EPI_GELU) && bn == 256)) ? 1 : 0;
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int CTAS = 1>
 static int set_attr() {
   static bool done = false;
   if (!done) {
-    constexpr int W = epi_warps<BN, KIND>();
-    const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, W, KIND>::SMEM_BYTES);
+    constexpr int W = epi_warps<BN, KIND, CTAS>();
+    using C = GemmCfg<BN, W, KIND, CTAS>;
+    const cudaError_t err = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, KIND, W, CTAS>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (err != cudaSuccess) {
-      fprintf(stderr, "streamflow: gemm<%d,%d> smem attribute (%d B) failed: %s\n", BN, KIND, GemmCfg<BN, W, KIND>::SMEM_BYTES,
+      fprintf(stderr, "streamflow: gemm<%d,%d,%d> smem attribute (%d B) failed: %s\n", BN, KIND, CTAS, C::SMEM_BYTES,
               cudaGetErrorString(err));
       return SF_ERR_CUDA;
     }
@@ -129,6 +134,7 @@ int prepare_gemm_kernels() {
   rc |= set_attr<256, EPI_BF16>();
   rc |= set_attr<256, EPI_GELU>();
   rc |= set_attr<192, EPI_QKV>();
+  rc |= set_attr<192, EPI_QKV, 2>();
   rc |= set_attr<128, EPI_QKV>();
   rc |= set_attr<384, EPI_RES_LN>();
   rc |= set_attr<144, EPI_QKV>();
@@ -149,18 +155,40 @@ static int sm_count() {
   return n;
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int CTAS = 1>
 static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams& ep, cudaStream_t st) {
-  constexpr int W = epi_warps<BN, KIND>();
-  using C = GemmCfg<BN, W, KIND>;
+  constexpr int W = epi_warps<BN, KIND, CTAS>();
+  using C = GemmCfg<BN, W, KIND, CTAS>;
   if (K % C::BK) return SF_ERR_PARAMETER;
-  if (set_attr<BN, KIND>() != SF_OK) return SF_ERR_CUDA;
+  if (C::B_RES && K != C::KB_RES * C::BK) return SF_ERR_PARAMETER;
+  if (set_attr<BN, KIND, CTAS>() != SF_OK) return SF_ERR_CUDA;
   const int tiles = (N / BN) * ((M + C::BM - 1) / C::BM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   EpiParams e = ep;
   e.M = M;
   cudaError_t err;
-  if constexpr (KIND == EPI_RES_LN2) {
+  if constexpr (CTAS == 2) {
+    // pairs: a multiple of N / BN so every pair keeps one column slice (B resident)
+    const int num_n = N / BN, pair_tiles = num_n * ((M + 2 * C::BM - 1) / (2 * C::BM));
+    int pairs = sm_count() / 2;
+    if (pairs > pair_tiles) pairs = pair_tiles;
+    pairs -= pairs % num_n;
+    if (pairs < num_n) pairs = num_n;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W, CTAS>, maps, N, K, e);
+    if (err == cudaSuccess) err = cudaGetLastError();
+  } else if constexpr (KIND == EPI_RES_LN2) {
     // one cluster of XCH_CL CTAs per row tile in flight: grid = whole clusters
     cudaLaunchConfig_t cfg = {};
     const int rows = (M + C::BM - 1) / C::BM, max_cl = sm_count() / XCH_CL;
@@ -193,8 +221,12 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
 
 
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
-                cudaStream_t st) {
+                cudaStream_t st, int ctas) {
   if (K % 32 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
+  if (ctas == 2) {
+    if (bn == 192 && kind == EPI_QKV) return launch_one<192, EPI_QKV, 2>(maps, M, N, K, ep, st);
+    return SF_ERR_PARAMETER;
+  }
 #define SF_CASE(BN_, KIND_) \
   if (bn == BN_ && kind == KIND_) return launch_one<BN_, KIND_>(maps, M, N, K, ep, st);
   SF_CASE(128, EPI_F32)

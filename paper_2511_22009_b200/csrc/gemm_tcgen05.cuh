@@ -81,11 +81,18 @@ struct GemmCfg {
   static constexpr int BK = BN > 256 ? 32 : 64;  // K elements per stage (64 B / 128 B rows)
   static constexpr int SWZ = BK * 2;             // swizzle width of the operand tiles (bytes)
   static constexpr int A_BYTES = BM * BK * 2;
-  // CTAS = 2: a cluster pair computes a 256 x BN tile with cta_group::2 MMAs; each CTA
-  // holds its 128 A rows and BN/2 B rows (the pair MMA reads B from both)
+  // CTAS = 2: a cluster pair computes 256 x BN tiles with cta_group::2 MMAs; each CTA
+  // holds its 128 A rows and BN/2 B rows (the pair MMA reads B from both).  The pair keeps
+  // one column slice n for its whole life and its half of that B slice stays RESIDENT in
+  // smem (K = KB_RES * BK), so only A streams through the ring: per 128 x BN tile a CTA
+  // pulls 96 KB of A from L2 instead of 96 KB of A + 144 KB of B (the single-CTA QKV GEMM
+  // waits on its operand ring, not on the tensor pipe or the epilogue: ncu, profiles/r02).
+  static constexpr bool B_RES = CTAS == 2;
+  static constexpr int KB_RES = 6;  // resident K blocks (K = 384, the DiT-S/2 hidden size)
   static constexpr int B_ROWS = BN / CTAS;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BRES_BYTES = B_RES ? KB_RES * B_BYTES : 0;
+  static constexpr int STAGE_BYTES = B_RES ? A_BYTES : A_BYTES + B_BYTES;
   static constexpr int MMA_N = BN > 256 ? BN / 2 : BN;  // UMMA N <= 256
   static constexpr int N_SPLIT = BN / MMA_N;
   static constexpr int B_BOX = B_ROWS > 256 ? B_ROWS / 2 : B_ROWS;  // TMA box rows <= 256
@@ -106,15 +113,16 @@ struct GemmCfg {
   static constexpr bool NARROW = LN_RING || ((KIND == EPI_BF16 || KIND == EPI_GELU) && EPI_WARPS == 16);
   static constexpr int OUT_BUF = BN == 144 ? 5120 : NARROW ? 2048 : 4096;
   // RES_LN(2): one buffer per chunk; QKV (head dim 64): 3 store buffers per warp
-  static constexpr int OUT_NBUF = LN_RING ? BN / (EPI_WARPS / 4) / 32 : (KIND == EPI_QKV && BN == 192) ? 3 : 2;
+  static constexpr int OUT_NBUF =
+      LN_RING ? BN / (EPI_WARPS / 4) / 32 : (KIND == EPI_QKV && BN == 192 && TILE_GROUPS == 1) ? 3 : 2;
   static constexpr int OUT_BYTES = EPI_WARPS * OUT_NBUF * OUT_BUF;
   static constexpr int RBAR_BYTES = EPI_WARPS * 4 * 8;  // residual-chunk barriers (one per staging buffer)
   // RES_LN2 exchange: [tile parity][pass][source CTA][column group][128 rows] floats
   static constexpr int XCH_BYTES = KIND == EPI_RES_LN2 ? 2 * 2 * XCH_CL * 2 * 128 * 4 : 0;
   static constexpr int FIXED = 1024 + 256 + RED_BYTES + VEC_BYTES + OUT_BYTES + RBAR_BYTES + XCH_BYTES;
-  static constexpr int STAGES_FIT = (227 * 1024 - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES_FIT = (227 * 1024 - FIXED - BRES_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int SMEM_BYTES = FIXED + STAGES * STAGE_BYTES;
+  static constexpr int SMEM_BYTES = FIXED + STAGES * STAGE_BYTES + BRES_BYTES;
   static_assert(STAGES >= 3, "pipeline too shallow");
   static_assert(MMA_N % 16 == 0 && MMA_N <= 256, "bad MMA N");
   static_assert(B_BOX <= 256, "bad box");
@@ -198,8 +206,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sOut = smem;                             // [EPI_WARPS][OUT_NBUF][OUT_BUF]   (1024-aligned)
   uint8_t* sA = sOut + C::OUT_BYTES;                // [STAGES][A_BYTES]
-  uint8_t* sB = sA + C::STAGES * C::A_BYTES;        // [STAGES][B_BYTES]
-  float* red = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);  // [2][8 warps][32]
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;        // [STAGES][B_BYTES] (B_RES: [KB_RES][B_BYTES])
+  float* red = reinterpret_cast<float*>(sB + (C::B_RES ? C::BRES_BYTES : C::STAGES * C::B_BYTES));  // [2][8 warps][32]
   float* vecs = red + C::RED_BYTES / 4;                                // [2][4][BN]
   uint64_t* bars = reinterpret_cast<uint64_t*>(vecs + C::VEC_BYTES / 4);
   uint64_t* full = bars;
@@ -210,6 +218,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
   uint64_t* rbar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [EPI_WARPS][3]
   float* xch = reinterpret_cast<float*>(rbar + EPI_WARPS * 4);  // RES_LN2 exchange
   uint64_t* xbar = tempty + C::ACC_STAGES + 1;                   // RES_LN2: [parity][pass], one arrive per CTA
+  uint64_t* bfull = xbar;                                        // B_RES: both halves of the resident B landed (leader)
   constexpr bool CLUSTER = KIND == EPI_RES_LN2;
 
   const uint32_t warp = warp_id();
@@ -231,13 +240,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     return CLUSTER ? tile * C::BM : TWO_SM ? (2 * (tile / num_n) + (int)crank) * C::BM : (tile / num_n) * C::BM;
   };
   auto tile_n0 = [&](int tile) { return CLUSTER ? (int)crank * BN : (tile % num_n) * BN; };
-  // epilogue -> MMA accumulator release (2-SM: both CTAs' epilogues arrive on the leader's barrier)
+  // epilogue -> MMA accumulator release (2-SM: one arrival per epilogue warp of both CTAs on the
+  // leader's barrier, cta-scope semantics as in the block tail: the TMEM reads are complete
+  // (tcgen05.wait::ld) before the arrive)
   auto acc_release = [&](uint32_t a) {
     tc_fence_before();
-    if constexpr (TWO_SM)
-      mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[a]), 0));
-    else
+    if constexpr (TWO_SM) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_u32(&tempty[a]), 0))
+                     : "memory");
+      __syncwarp();
+    } else {
       mbar_arrive(&tempty[a]);
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -249,8 +265,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     }
     for (int a = 0; a < C::ACC_STAGES; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CTAS * EPI_WARPS * 32 / C::TILE_GROUPS);
+      mbar_init(&tempty[a], TWO_SM ? CTAS * EPI_WARPS / C::TILE_GROUPS : EPI_WARPS * 32 / C::TILE_GROUPS);
     }
+    if constexpr (C::B_RES) mbar_init(bfull, 1);
     if constexpr (KIND == EPI_RES_LN || KIND == EPI_RES || KIND == EPI_RES_LN2)
       for (int i = 0; i < EPI_WARPS * 4; ++i) mbar_init(&rbar[i], 1);
     if constexpr (CLUSTER)
@@ -273,6 +290,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     if (lane == 0) {
       // ---------------- TMA producer (ring continues across tiles)
       uint32_t it = 0;
+      if constexpr (C::B_RES) {
+        // the pair's column slice is fixed (the host sizes the grid to a multiple of N / BN
+        // pairs): this CTA's half of B, all K blocks, once; both halves complete on the leader
+        if (t_first < t_limit) {
+          if (leader) mbar_expect_tx(bfull, 2 * C::BRES_BYTES);
+          for (int kb = 0; kb < C::KB_RES; ++kb)
+            tma_load_2d_2sm(sB + kb * C::B_BYTES, &maps.b, mapa_shared(smem_u32(bfull), 0), kb * C::BK,
+                            tile_n0(t_first) + (int)crank * C::B_ROWS);
+        }
+      }
       for (int tile = t_first; tile < t_limit; tile += t_stride) {
         const int m0 = tile_m0(tile), n0 = tile_n0(tile);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -283,7 +310,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
             const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
             if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
             tma_load_2d_2sm(sA + s * C::A_BYTES, &maps.a, fb, kb * C::BK, m0);
-            tma_load_2d_2sm(sB + s * C::B_BYTES, &maps.b, fb, kb * C::BK, n0 + (int)crank * C::B_ROWS);
+            if constexpr (!C::B_RES)
+              tma_load_2d_2sm(sB + s * C::B_BYTES, &maps.b, fb, kb * C::BK, n0 + (int)crank * C::B_ROWS);
             continue;
           }
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
@@ -304,6 +332,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     const uint64_t a_desc0 = kmajor_desc<C::SWZ>(smem_u32(sA));
     const uint64_t b_desc0 = kmajor_desc<C::SWZ>(smem_u32(sB));
     uint32_t it = 0, local = 0;
+    if constexpr (C::B_RES) {
+      if (leader && t_first < t_limit) {
+        mbar_wait(bfull, 0);
+        tc_fence_after();
+      }
+    }
     for (int tile = t_first; tile < ((TWO_SM && !leader) ? t_first : t_limit); tile += t_stride, ++local) {
       const uint32_t acc = local % C::ACC_STAGES, aph = (local / C::ACC_STAGES) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
@@ -315,7 +349,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint64_t ad = a_desc0 + (uint64_t)((s * C::A_BYTES) >> 4);
-        const uint64_t bd = b_desc0 + (uint64_t)((s * C::B_BYTES) >> 4);
+        const uint64_t bd = b_desc0 + (uint64_t)(((C::B_RES ? kb : (int)s) * C::B_BYTES) >> 4);
         if (elect_one()) {
           if constexpr (TWO_SM) {
 #pragma unroll

@@ -15,7 +15,9 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
                       uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128);
 int gemm_bk(int bn);
 int gemm_b_box_rows(int bn);
-int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn);
+// ctas = 2: pair tiles (each CTA loads BN / 2 rows of W per box)
+int make_operand_maps(GemmMaps* m, const void* A, int64_t M, int64_t K, const void* W, int64_t N, int bn,
+                      int ctas = 1);
 int make_out_map(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
 int make_out_map32(CUtensorMap* m, const void* D, int64_t rows, int64_t cols);
 int gemm_narrow_out(int bn, int kind);
@@ -26,7 +28,7 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 int prepare_gemm_kernels();
 int prepare_attn_kernel();
 int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, const EpiParams& ep,
-                cudaStream_t st);
+                cudaStream_t st, int ctas = 1);
 
 struct AttnMaps {
   CUtensorMap q, qh, k, kh, v;  // qh/kh: head-dim elements 64..79 (head dim 72 only)
@@ -37,6 +39,7 @@ int make_attn_maps(AttnMaps* m, const void* q, const void* k, const void* vt, in
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st);
 
 int qkv_bn64();
+int qkv_ctas(int64_t K);  // 2: the head-dim-64 QKV runs on CTA pairs with B resident (K = 384)
 // csrc/block_tail.cu (M % 256 == 0, T % 128 == 0)
 int launch_block_tail(const void* attn, const void* wproj, const float* bproj, const void* w1, const void* w2,
                            const float* b1, const float* b2, __nv_bfloat16* xres, __nv_bfloat16* xmod_out,
