@@ -49,6 +49,53 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, int64_t gen, int64
   return (lane & 1) ? rad * s : rad * c;
 }
 
+// philox_normal for the final layer's 8 elements per lane (idx[nt][i], see final_layer_mma_kernel):
+// the four lanes 8k + (c & 1) + {0, 2, 4, 6} own the four samples of one Philox counter
+// (idx >> 2) for every element slot u = 4 nt + i, so lane r = 2 (g & 1) + (c >> 1) of the group
+// runs the generator for slots 2r, 2r + 1 (all four samples each) and the samples are
+// exchanged with shuffles: 2 Philox calls per lane instead of 8, the same values.
+__device__ __forceinline__ void philox_normal_group8(uint64_t seed, int64_t gen, const int64_t (&idx)[2][4], int lane,
+                                                     float (&out)[2][4]) {
+  const int g = lane >> 2, c = lane & 3;
+  const int r = 2 * (g & 1) + (c >> 1);  // this lane's sample within a counter = idx % 4
+  const int base = lane & ~0x6;  // lane of r = 0 in this group: 8k + (c & 1)
+  float v[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    // slot u = 2r + h: every lane computes its own slot's counter from its own idx (the four lanes
+    // of the group hold the same counter for a given slot)
+    int64_t myidx = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u == 2 * r + h) myidx = idx[u >> 2][u & 3];
+    const uint4 q = philox4x32(make_uint4((uint32_t)(myidx >> 2), (uint32_t)gen, (uint32_t)(gen >> 32), 0x5f1u),
+                               make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+      const uint32_t a = pr ? q.z : q.x, b = pr ? q.w : q.y;
+      const float u1 = ((float)a + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+      const float u2 = (float)b * 2.3283064365386963e-10f;
+      const float rad = sqrtf(-2.0f * __logf(u1));
+      float sn, cs;
+      __sincosf(6.283185307179586f * u2, &sn, &cs);
+      v[h][2 * pr] = rad * cs;
+      v[h][2 * pr + 1] = rad * sn;
+    }
+  }
+  // slot u lives in lane base + 2 (u >> 1) (its r = u >> 1), register v[u & 1][.]; lane r needs sample r
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int src = base + 2 * (u >> 1);
+    float got = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float t = __shfl_sync(0xffffffffu, v[u & 1][k], src);
+      if (k == r) got = t;
+    }
+    out[u >> 2][u & 3] = got;
+  }
+}
+
 // Where a network row takes its inputs from (stream mode vs direct forward).
 struct RowSrc {
   const int64_t* row_info;  // stream mode: ring bookkeeping; nullptr in direct mode
@@ -390,149 +437,122 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
-// Output side of the final layer, shared by the FMA and the mma.sync kernels.
-struct FinalOut {
-  int HW, P, C;
-  float* eps_out;      // direct mode
-  const int64_t* ctl;  // stream mode from here on
-  int n;
-  int64_t m;
-  const double* stage_params;
-  const int64_t* row_info;
-  float* x_ring;
-  const float* noise_in;
-  uint64_t noise_seed;
-  float* frames_out;
-  int64_t* frame_ids;
-};
-
-// eps of feature f of token tau of latent row lr -> unpatchify, then either store it
-// (direct) or apply the Euler step + emit + refill of that latent element (stream).
-template <bool STREAM>
-__device__ __forceinline__ void final_element(const FinalOut& o, int64_t j, int64_t lr, int tau, int gw, int f, float e) {
-  const int HW = o.HW, P = o.P, C = o.C;
-  const int64_t D = (int64_t)C * HW * HW;
-  const int pi = tau / gw, pj = tau % gw;
-  // unpatchify: feature f = (p*P + q)*C + c  ->  pixel (pi*P + p, pj*P + q) of channel c
-  const int c = f % C, q = (f / C) % P, p = f / (C * P);
-  const int64_t idx = (int64_t)c * HW * HW + (int64_t)(pi * P + p) * HW + (pj * P + q);
-  if constexpr (!STREAM) {
-    o.eps_out[lr * D + idx] = e;
-  } else {
-    const int n = o.n;
-    const int64_t stage = o.row_info[lr * 4 + 0];
-    const int64_t g = o.row_info[lr * 4 + 1];
-    const bool active = o.row_info[lr * 4 + 2] != 0;
-    const int64_t s = o.row_info[lr * 4 + 3];
-    const int64_t k = lr % n;
-    const bool refill_slot = (k == (j + 1) % n);
-    const bool admit = refill_slot && (j + 1 < o.m);
-    const bool retiring = active && (stage + 1 == n);
-    if (refill_slot && tau == 0 && f == 0) o.frame_ids[s] = retiring ? g : -1;
-    float* xr = o.x_ring + lr * D;
-    const float noise =
-        admit ? (o.noise_in ? o.noise_in[s * D + idx] : philox_normal(o.noise_seed + (uint64_t)s, j + 1, idx)) : 0.0f;
-    if (active) {
-      const double* pp = o.stage_params + stage * SF_PARAM_STRIDE;
-      const float lam = __double2float_rn(pp[SF_P_LAMBDA_T]), eta = __double2float_rn(pp[SF_P_ETA_T]);
-      const float span = __double2float_rn(pp[SF_P_SPAN]), dt = __double2float_rn(pp[SF_P_DT]);
-      const bool at_end = pp[SF_P_AT_END] != 0.0;
-      const float xo = xr[idx];
-      // velocity.py:125-130 in fp32
-      const float x_pred = __fadd_rn(__fmul_rn(lam, xo), __fmul_rn(eta, e));
-      const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo), span);
-      const float xn = __fadd_rn(xo, __fmul_rn(dt, v));
-      if (retiring) o.frames_out[s * D + idx] = xn;
-      xr[idx] = admit ? noise : xn;
-    } else if (admit) {
-      xr[idx] = noise;
-    }
-  }
-}
-
-// One warp per group of 4 consecutive tokens (grid-stride).  Lane partial dot
-// products over its 4 x U columns for all 4 tokens x 16 output features (each
-// float4 weight read serves the 4 tokens), then a butterfly reduce-scatter
-// (31 shuffles of 64 -> 2 values per lane): lane ends up owning token lane/8,
-// features 2 (lane%8) and 2 (lane%8) + 1, i.e. two latent pixels.
-// One reduce-scatter round: lanes with bit `o` keep the upper half of the live
-// 2H values, the others the lower half; each adds its partner's copy.
-template <int H, int N>
-__device__ __forceinline__ void bfly_round(float (&a)[N], int o, int lane) {
-  const bool hi = (lane & o) != 0;
-#pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const float send = hi ? a[i] : a[i + H];
-    const float keep = hi ? a[i + H] : a[i];
-    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-  }
-}
-
-
 // Same layer on the warp-level tensor path (mma.sync m16n8k16, bf16 in, fp32
 // accumulate): one warp per 16 consecutive tokens (T % 16 == 0), N = 16 output
 // features as two n8 tiles, K = HID in 16-wide steps.  The projection is ~0.4% of the
-// network's FLOPs, so the legacy HMMA rate is ample; what matters is that xmod
-// (the kernel's only large input, T*HID bf16 per row) streams at HBM rate: each
-// lane reads 16-byte runs, K permuted so that a lane's run feeds its own fragments
-// (logical k {2c, 2c+1, 2c+8, 2c+9} of a 16-step <-> physical 8c + {0, 1, 2, 3},
-// the same map for A and B, so the dot products are unchanged).  Fragment
-// ownership after the MMA: lane (g = lane/4, c = lane%4) holds tokens g and g+8,
-// features {2c, 2c+1} and {8+2c, 9+2c}.
-constexpr int FINAL_WPAD = 64;  // bytes of padding per smem weight row (conflict-free LDS.128)
+// network's FLOPs, so the legacy HMMA rate is ample; what matters is that xmod (the
+// kernel's only large input, T*HID bf16 per row) streams at HBM rate.  Each warp owns a
+// two-deep ring of 16-token tiles in shared memory filled by TMA (one box per tile) and
+// completing on a per-buffer mbarrier: the loads of the next two groups are in flight while
+// the warp runs the projection and the Euler/emit/refill epilogue of the current one, and
+// the epilogue's own loads (ring row, noise, stage parameters) are issued before the tile
+// wait.  The tensor map views a token row as NSEG = HID/192 segments of 192 elements and
+// the box is 208 elements wide: TMA zero-fills the 16 out-of-bounds elements, so every
+// staged segment is 416 B and consecutive token rows start 64 B apart modulo 128 B -- the
+// fragment loads of a quarter-warp (two token rows) are conflict-free without a per-row
+// copy.  The weights use the same layout.  K is permuted so that a lane's 16-byte run feeds
+// its own fragments (logical k {2c, 2c+1, 2c+8, 2c+9} of a 16-step <-> physical 8c + {0..3},
+// the same map for A and B, so the dot products are unchanged).  Fragment ownership after
+// the MMA: lane (g = lane/4, c = lane%4) holds tokens g and g+8, features {2c, 2c+1} and
+// {8+2c, 9+2c}.
+template <int HID>
+struct FinalCfg {
+  static constexpr int PK = 16;
+  static constexpr int SEG = 192, SEG_BOX = 208;       // elements per segment / per staged segment
+  static constexpr int NSEG = HID / SEG;
+  static constexpr int SROW = SEG_BOX * 2;             // staged segment (bytes)
+  static constexpr int TROW = NSEG * SROW;             // staged token / weight row (bytes)
+  static constexpr int TILE = 16 * TROW;
+  static constexpr int HEAD = ((PK * TROW + PK * 4 + (2 * 8 + 1) * 8) + 127) / 128 * 128;  // weights, bias, barriers
+  static_assert(HID % SEG == 0 && (TROW % 128) == 64, "token rows must alternate 64-byte bank halves");
+  // warps per CTA: two ring buffers per warp of 1 (2 with CFG: cond + uncond rows) tiles
+  static int warps(int tiles) {
+    const int w = (227 * 1024 - HEAD) / (2 * tiles * TILE);
+    return w > 8 ? 8 : (w < 1 ? 1 : w);
+  }
+  static size_t smem(int tiles) { return HEAD + (size_t)warps(tiles) * 2 * tiles * TILE; }
+};
+
+// [rows, HID] bf16 -> [rows * NSEG, 192] with 208-wide boxes of 16 * NSEG segment rows
+template <int HID>
+int make_final_map(CUtensorMap* m, const void* p, int64_t rows) {
+  using FC = FinalCfg<HID>;
+  return make_tmap_bf16_2d(m, p, FC::SEG, (uint64_t)rows * FC::NSEG, FC::SEG, FC::SEG_BOX, 16 * FC::NSEG, 0);
+}
 
 template <int HID, bool STREAM>
 __global__ void __launch_bounds__(256) final_layer_mma_kernel(
-    const __nv_bfloat16* __restrict__ xmod, const __nv_bfloat16* __restrict__ fw, const float* __restrict__ fb, int HW,
+    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, const float* __restrict__ fb, int HW,
     int P, int C, int64_t lat_rows, float* __restrict__ eps_out, const int64_t* __restrict__ ctl, int n, int64_t m,
     const double* __restrict__ stage_params, const int64_t* __restrict__ row_info, int cfg, float w,
     const double* __restrict__ w_streams, float* __restrict__ x_ring, const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
     int64_t* __restrict__ frame_ids, int64_t total_tokens) {
-  constexpr int PK = 16;
-  constexpr int WROW = HID * 2 + FINAL_WPAD;  // bytes
-  extern __shared__ __align__(16) uint8_t fsm[];  // [PK][WROW] bf16 weights, then bias[PK]
-  float* sbias = reinterpret_cast<float*>(fsm + PK * WROW);
-  for (int idx = threadIdx.x; idx < PK * HID / 8; idx += blockDim.x) {
-    const int r = idx / (HID / 8), c8 = idx % (HID / 8);
-    *reinterpret_cast<uint4*>(fsm + r * WROW + c8 * 16) = reinterpret_cast<const uint4*>(fw)[idx];
+  using FC = FinalCfg<HID>;
+  constexpr int PK = FC::PK, TROW = FC::TROW, SROW = FC::SROW;
+  extern __shared__ __align__(128) uint8_t fsm[];  // [PK][TROW] bf16 weights, bias[PK], barriers, tile rings
+  float* sbias = reinterpret_cast<float*>(fsm + PK * TROW);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fsm + PK * TROW + PK * 4);  // [warp][2], then the weight barrier
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  const int WARPS = blockDim.x >> 5;
+  const int NT = (STREAM && cfg) ? 2 : 1;  // tiles per group: cond (+ uncond) rows
+  uint8_t* ring = fsm + FC::HEAD + (size_t)warp * 2 * NT * FC::TILE;
+  uint64_t* bar = bars + 2 * warp;
+  uint64_t* wbar = bars + 2 * WARPS;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmX);
+    mbar_init(wbar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(wbar, (uint32_t)(PK * TROW));
+    tma_load_2d(fsm, &tmW, wbar, 0, 0);
+  }
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
   }
   if (threadIdx.x < PK) sbias[threadIdx.x] = fb[threadIdx.x];
   __syncthreads();
-  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const int gw = HW / P, T = gw * gw;
   int64_t j = 0;
   if constexpr (STREAM) j = ctl[1];
-  const uint8_t* wrow0 = fsm + g * WROW + 16 * c;        // feature g      (n-tile 0)
-  const uint8_t* wrow1 = fsm + (g + 8) * WROW + 16 * c;  // feature g + 8  (n-tile 1)
+  const uint8_t* wrow0 = fsm + g * TROW + 16 * c;        // feature g      (n-tile 0)
+  const uint8_t* wrow1 = fsm + (g + 8) * TROW + 16 * c;  // feature g + 8  (n-tile 1)
+  const int64_t groups = total_tokens / 16;
+  const int64_t gstride = (int64_t)gridDim.x * WARPS;
 
+  // the 16 token rows of group grp (net rows: cond = lr (+ lat_rows with CFG), uncond = lr) -> buffer b
+  auto issue = [&](int64_t grp, int b) {
+    if (lane == 0) {
+      const int64_t tok0 = grp * 16, lr = tok0 / T;
+      const int tau0 = (int)(tok0 % T);
+      mbar_expect_tx(&bar[b], (uint32_t)(NT * FC::TILE));
+      for (int t = 0; t < NT; ++t) {
+        const int64_t net_row = (t == 0 && NT == 2) ? lr + lat_rows : lr;
+        tma_load_2d(ring + (b * NT + t) * FC::TILE, &tmX, &bar[b], 0, (int)((net_row * T + tau0) * FC::NSEG));
+      }
+    }
+    __syncwarp();
+  };
   // acc[nt][0..1]: token g, features 8nt + 2c + {0,1}; acc[nt][2..3]: token g + 8
-  auto project = [&](int64_t net_row, int tau0, float (&acc)[2][4]) {
+  auto project = [&](const uint8_t* tile, float (&acc)[2][4]) {
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
-    const uint8_t* a0 = reinterpret_cast<const uint8_t*>(xmod + (net_row * T + tau0 + g) * HID) + 16 * c;
-    const uint8_t* a1 = a0 + 8 * HID * 2;
-    constexpr int NCH = HID / 32;  // 32 K elements (two k-steps) per 16-byte lane run
-    constexpr int UNR = 6;
-    static_assert(NCH % UNR == 0, "chunking");
-#pragma unroll 1
-    for (int ch0 = 0; ch0 < NCH; ch0 += UNR) {
-      uint4 xa[UNR], xb[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        xa[u] = ldg_stream_u4(a0 + 64 * (ch0 + u));
-        xb[u] = ldg_stream_u4(a1 + 64 * (ch0 + u));
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const uint4 b0 = *reinterpret_cast<const uint4*>(wrow0 + 64 * (ch0 + u));
-        const uint4 b1 = *reinterpret_cast<const uint4*>(wrow1 + 64 * (ch0 + u));
-        mma_bf16_16816(acc[0], xa[u].x, xb[u].x, xa[u].y, xb[u].y, b0.x, b0.y);
-        mma_bf16_16816(acc[1], xa[u].x, xb[u].x, xa[u].y, xb[u].y, b1.x, b1.y);
-        mma_bf16_16816(acc[0], xa[u].z, xb[u].z, xa[u].w, xb[u].w, b0.z, b0.w);
-        mma_bf16_16816(acc[1], xa[u].z, xb[u].z, xa[u].w, xb[u].w, b1.z, b1.w);
-      }
+    const uint8_t* a0 = tile + g * TROW + 16 * c;
+    const uint8_t* a1 = a0 + 8 * TROW;
+    constexpr int NCH = HID / 32;  // 32 K elements (two k-steps) per 16-byte lane run; 6 per segment
+#pragma unroll 6
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int off = (ch / 6) * SROW + (ch % 6) * 64;
+      const uint4 xa = *reinterpret_cast<const uint4*>(a0 + off);
+      const uint4 xb = *reinterpret_cast<const uint4*>(a1 + off);
+      const uint4 b0 = *reinterpret_cast<const uint4*>(wrow0 + off);
+      const uint4 b1 = *reinterpret_cast<const uint4*>(wrow1 + off);
+      mma_bf16_16816(acc[0], xa.x, xb.x, xa.y, xb.y, b0.x, b0.y);
+      mma_bf16_16816(acc[1], xa.x, xb.x, xa.y, xb.y, b1.x, b1.y);
+      mma_bf16_16816(acc[0], xa.z, xb.z, xa.w, xb.w, b0.z, b0.w);
+      mma_bf16_16816(acc[1], xa.z, xb.z, xa.w, xb.w, b1.z, b1.w);
     }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -544,23 +564,71 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     }
   };
 
-  const FinalOut o{HW, P, C, eps_out, ctl, n, m, stage_params, row_info, x_ring, noise_in, noise_seed, frames_out,
-                   frame_ids};
-  const int64_t groups = total_tokens / 16;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t grp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; grp < groups; grp += wstride) {
-    const int64_t tok0 = grp * 16;
-    const int64_t lr = tok0 / T;
+  const int64_t D = (int64_t)C * HW * HW;
+  const int64_t gw0 = (int64_t)blockIdx.x * WARPS + warp;
+  if (gw0 < groups) issue(gw0, 0);
+  if (gw0 + gstride < groups) issue(gw0 + gstride, 1);
+  int it = 0;
+  for (int64_t grp = gw0; grp < groups; grp += gstride, ++it) {
+    const int b = it & 1;
+    const int64_t tok0 = grp * 16, lr = tok0 / T;
     const int tau0 = (int)(tok0 % T);
-    float e[2][4];
-    project(STREAM && cfg ? lr + lat_rows : lr, tau0, e);
+    // this lane's 8 latent elements u = 4 nt + i: token tau0 + g + 8 (i >> 1), feature
+    // f = 8 nt + 2c + (i & 1) = (p P + q) C + ch with P = 2, C = 4 (sf_dit_create) -> pixel
+    // (2 pi + nt, 2 pj + (c >> 1)) of channel 2 (c & 1) + (i & 1).  The 16 tokens of a group share
+    // pi (gw % 16 == 0), so only the group's first token is divided.
+    const int pi0 = tau0 / gw, pj0 = tau0 - pi0 * gw;
+    const int64_t HW2 = (int64_t)HW * HW;
+    int64_t idx[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        idx[nt][i] = (2 * (c & 1) + (i & 1)) * HW2 + (int64_t)(2 * pi0 + nt) * HW + 2 * (pj0 + g + 8 * (i >> 1)) +
+                     (c >> 1);
+    // stream epilogue inputs, loaded before the tile wait (velocity.py:125-130 Euler,
+    // pipeline.py:172-207 emit / admit)
+    bool active = false, admit = false, retiring = false, at_end = false;
+    float lam = 0.f, eta = 0.f, span = 1.f, dt = 0.f, wl = w;
+    int64_t s = 0;
+    float xo[2][4], nz[2][4];
     if constexpr (STREAM) {
+      const int64_t stage = row_info[lr * 4 + 0], gen = row_info[lr * 4 + 1];
+      active = row_info[lr * 4 + 2] != 0;
+      s = row_info[lr * 4 + 3];
+      const bool refill_slot = (lr % n) == (j + 1) % n;
+      admit = refill_slot && (j + 1 < m);
+      retiring = active && (stage + 1 == n);
+      if (refill_slot && tau0 == 0 && lane == 0) frame_ids[s] = retiring ? gen : -1;
+      if (active) {
+        const double* pp = stage_params + stage * SF_PARAM_STRIDE;
+        lam = __double2float_rn(pp[SF_P_LAMBDA_T]);
+        eta = __double2float_rn(pp[SF_P_ETA_T]);
+        span = __double2float_rn(pp[SF_P_SPAN]);
+        dt = __double2float_rn(pp[SF_P_DT]);
+        at_end = pp[SF_P_AT_END] != 0.0;
+      }
       // per-stream guidance: a stream with w == 1 takes the conditional eps as is (apply_cfg is
       // the identity for it, models.py:254-255; row independence makes its cond row exact)
-      const float wl = w_streams ? (float)w_streams[row_info[lr * 4 + 3]] : w;
-      if (cfg && wl != 1.0f) {
+      if (w_streams) wl = (float)w_streams[s];
+      const float* xr = x_ring + lr * D;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          xo[nt][i] = active ? xr[idx[nt][i]] : 0.f;
+          nz[nt][i] = (admit && noise_in) ? noise_in[s * D + idx[nt][i]] : 0.f;
+        }
+      if (admit && !noise_in) philox_normal_group8(noise_seed + (uint64_t)s, j + 1, idx, lane, nz);
+    }
+    if (it == 0) mbar_wait(wbar, 0);  // weights staged
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    float e[2][4];
+    project(ring + b * NT * FC::TILE, e);
+    if constexpr (STREAM) {
+      if (NT == 2 && wl != 1.0f) {
         float eu[2][4];
-        project(lr, tau0, eu);
+        project(ring + (b * NT + 1) * FC::TILE, eu);
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
@@ -568,11 +636,28 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
             e[nt][i] = __fadd_rn(eu[nt][i], __fmul_rn(wl, __fsub_rn(e[nt][i], eu[nt][i])));
       }
     }
+    __syncwarp();  // every lane's fragment loads of buffer b are done: refill it
+    if (grp + 2 * gstride < groups) issue(grp + 2 * gstride, b);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        final_element<STREAM>(o, j, lr, tau0 + g + 8 * (i >> 1), gw, 8 * nt + 2 * c + (i & 1), e[nt][i]);
+      for (int i = 0; i < 4; ++i) {
+        if constexpr (!STREAM) {
+          eps_out[lr * D + idx[nt][i]] = e[nt][i];
+        } else {
+          float* xr = x_ring + lr * D + idx[nt][i];
+          if (active) {
+            // velocity.py:125-130 in fp32
+            const float x_pred = __fadd_rn(__fmul_rn(lam, xo[nt][i]), __fmul_rn(eta, e[nt][i]));
+            const float v = at_end ? 0.0f : __fdiv_rn(__fsub_rn(x_pred, xo[nt][i]), span);
+            const float xn = __fadd_rn(xo[nt][i], __fmul_rn(dt, v));
+            if (retiring) frames_out[s * D + idx[nt][i]] = xn;
+            *xr = admit ? nz[nt][i] : xn;
+          } else if (admit) {
+            *xr = nz[nt][i];
+          }
+        }
+      }
   }
 }
 
@@ -612,6 +697,7 @@ struct sf_dit {
   GemmMaps g_ada;                                  // TMA descriptors per GEMM call site
   std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
   AttnMaps attn_maps;
+  CUtensorMap fin_x, fin_w;  // final layer: xmod / final weight rows as 208-wide segment boxes
   // One instantiated graph per distinct argument set of sf_dit_stream_step: every pointer and
   // value the capture bakes into a launch is part of the key, so a replay is always the launch
   // sequence an eager call with the same arguments would enqueue.  Owners release their graphs
@@ -797,12 +883,13 @@ static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int6
                          const float* noise_in, uint64_t noise_seed, float* frames_out, int64_t* frame_ids,
                          int64_t tokens, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
-  const __nv_bfloat16* fw = (const __nv_bfloat16*)h->w.final_w;
-  const int PK = c.in_ch * c.patch * c.patch;
-  const size_t sm = (size_t)PK * (c.hidden * 2 + FINAL_WPAD) + PK * sizeof(float);
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + 7) / 8, 148 * 8);
+  const int tiles = (STREAM && cfg) ? 2 : 1;
+  const size_t sm = c.hidden == 384 ? FinalCfg<384>::smem(tiles) : FinalCfg<1152>::smem(tiles);
+  const int wpb = c.hidden == 384 ? FinalCfg<384>::warps(tiles) : FinalCfg<1152>::warps(tiles);
+  // persistent: one CTA per SM (the tile rings fill its shared memory), each warp walks groups
+  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, 148);
   auto fk = c.hidden == 384 ? final_layer_mma_kernel<384, STREAM> : final_layer_mma_kernel<1152, STREAM>;
-  fk<<<blocks, 256, sm, st>>>(h->xmod, fw, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
+  fk<<<blocks, 32 * wpb, sm, st>>>(h->fin_x, h->fin_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
                               stage_params, row_info, cfg, w, w_streams, x_ring, noise_in, noise_seed, frames_out,
                               frame_ids,
                               tokens);
@@ -872,6 +959,13 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     }
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens, c.hidden / c.heads);
+  if (c.hidden == 384) {
+    rc |= make_final_map<384>(&h->fin_x, h->xmod, max_rows * h->tokens);
+    rc |= make_final_map<384>(&h->fin_w, w->final_w, 16);
+  } else {
+    rc |= make_final_map<1152>(&h->fin_x, h->xmod, max_rows * h->tokens);
+    rc |= make_final_map<1152>(&h->fin_w, w->final_w, 16);
+  }
   if (rc != SF_OK) {
     delete h;
     return SF_ERR_CUDA;
@@ -885,6 +979,14 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
                        PatchMma<384>::SMEM);
   cudaFuncSetAttribute(patch_embed_ln_mma_kernel<1152>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        PatchMma<1152>::SMEM);
+  cudaFuncSetAttribute(final_layer_mma_kernel<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max(FinalCfg<384>::smem(1), FinalCfg<384>::smem(2)));
+  cudaFuncSetAttribute(final_layer_mma_kernel<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)FinalCfg<384>::smem(1));
+  cudaFuncSetAttribute(final_layer_mma_kernel<1152, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max(FinalCfg<1152>::smem(1), FinalCfg<1152>::smem(2)));
+  cudaFuncSetAttribute(final_layer_mma_kernel<1152, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)FinalCfg<1152>::smem(1));
   *out = h;
   return cuda_status();
 }

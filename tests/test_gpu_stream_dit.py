@@ -174,3 +174,28 @@ def test_dit_mixed_guidance_equals_separate_batches(setup):
         alone = sf.StreamBatch(model, sched, n, num_streams=1, cond=conds[s], seed=40 + s, m=m, dtype=np.float32)()
         for a, b in zip(mixed[s], alone[0]):
             assert a.id == b.id and np.array_equal(a.latent, b.latent), (s, a.id)
+
+
+@pytest.mark.parametrize("w", [1.0, 3.0])
+def test_device_noise_refill_equals_philox_fill(setup, w):
+    """noise='device': the final-layer kernel draws the admitted generation's noise itself (Philox
+    counters shared across lanes); the admitted ring rows must equal sf_philox_normal's output for
+    (seeds[0] + s, generation j + 1) element for element, with and without the CFG tile pair."""
+    sf, model = setup
+    from paper_2511_22009_b200 import _lib
+
+    S, n = 2, 4  # 16 network rows with CFG (the fixture's max_rows)
+    sched = sf.build_time_window_schedule(num_windows=3, inference_steps=n)
+    cond = sf.make_conditioning(np.ones(8), guidance_scale=w)
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=cond, seed=11, m=6, dtype=np.float32,
+                        noise="device", use_graph=False)
+    st = torch.cuda.current_stream().cuda_stream
+    ref = torch.empty(S, model.dim, dtype=torch.float32, device="cuda")
+    _lib.call("sf_philox_normal", ref.data_ptr(), S, model.dim, sb.noise_seed, 0, st)
+    ring = sb.x_ring.view(S, n, -1)
+    assert torch.equal(ring[:, 0], ref)  # generation 0 (reset)
+    for j in range(3):
+        sb.launch()
+        _lib.call("sf_philox_normal", ref.data_ptr(), S, model.dim, sb.noise_seed, j + 1, st)
+        torch.cuda.synchronize()
+        assert torch.equal(ring[:, (j + 1) % n], ref), j
