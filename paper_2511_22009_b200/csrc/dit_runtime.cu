@@ -218,77 +218,125 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 }
 
 
-// The same patch embed + LN1 modulate on the warp-level tensor path (mma.sync
-// m16n8k16): one warp per 16 consecutive tokens, K = 16 = the patch vector
-// (C=4, P=2), HID/8 n8 tiles.  x is fp32, so it enters as a bf16 hi/lo pair
-// (x = hi + lo to 2^-17 relative; two MMAs per tile) against the bf16 weights,
-// fp32 accumulate: the sum matches the FMA kernel to fp32 rounding.  Lane (g =
-// lane/4, c = lane%4) holds A pairs k = 2c, 2c+1 (channel c/2, patch row c%2: one
-// float2 of x) and k = 2c+8, 2c+9 (channel c/2 + 2), and after each MMA tokens g,
-// g+8 x fragment columns 2c, 2c+1 of each tile.  Output columns are permuted over
-// blocks of four tiles: fragment column 2c+e of tile q of block blk is hidden column
-// 32 blk + 8c + 2q + e, so a lane owns 8 consecutive columns per block (one 16-byte
-// bf16 run, two float4 of pos).  The B fragments (weight rows in that order) are
-// pre-arranged in smem as one uint2 per lane per tile (conflict-free LDS.64).  The
-// 16 residual rows (one contiguous 16*HID bf16 block in HBM) are staged in a padded
-// smem tile (row stride HID*2 + 64 B: a quarter-warp's 16-byte writes hit 32
-// distinct banks) with their row statistics, then written out as coalesced 256-byte
-// warp stores, and LN + modulate runs in that copy-out layout from the staged bf16
-// residual (no second projection).
+// Patch embed + LN1 modulate on the warp-level tensor path (mma.sync m16n8k16): one warp per
+// 16 consecutive tokens, K = 16 = the patch vector (C=4, P=2), HID/8 n8 tiles.  x is fp32, so
+// it enters as a bf16 hi/lo pair (x = hi + lo to 2^-17 relative; two MMAs per tile) against the
+// bf16 weights, fp32 accumulate.  Lane (g = lane/4, c = lane%4) holds A pairs k = 2c, 2c+1
+// (channel c/2, patch row c%2: one float2 of x) and k = 2c+8, 2c+9 (channel c/2 + 2), and
+// after each MMA tokens g, g+8 x fragment columns 2c, 2c+1 of each tile.  Output columns are
+// permuted over blocks of four tiles: fragment column 2c+e of tile q of block blk is hidden
+// column 32 blk + 8c + 2q + e, so a lane owns 8 consecutive columns per block (one 16-byte
+// bf16 run).  The B fragments (weight rows in that order) are pre-arranged in smem as one
+// uint2 per lane per tile (conflict-free LDS.64).
+//
+// Work split: CTA c owns the 16-token group tg = c % (T/16) of every latent row it visits
+// (rows c / (T/16), + CTAs / (T/16), ...; the host makes the grid a multiple of T/16), so the
+// group's slice of the positional table (16 x HID fp32, with the patch bias pre-added in the
+// reference's order) is loaded into shared memory ONCE per CTA instead of per group from L2
+// (the long-scoreboard stall that bounded the previous version).  The next group's x is
+// prefetched into registers.  The 16 residual rows are staged in shared memory as NSEG = HID/192
+// segments of 208 elements (416 B: consecutive rows alternate 64-byte bank halves, conflict-
+// free 16-byte writes) and leave by one TMA store (the 16 zero-padding elements of a segment
+// are out of bounds of the [tokens * NSEG, 192] tensor map, so they are not written); LN +
+// modulate runs in a copy-out layout from the staged bf16 residual (coalesced 8-byte lanes).
 template <int HID>
 struct PatchMma {
   static constexpr int NT = HID / 8;
-  static constexpr int WARPS = HID <= 384 ? 7 : 4;  // two CTAs per SM at hidden 384 (smem)
-  static constexpr int ROW = HID * 2 + 64;                 // staged row stride, bytes
-  static constexpr int WBUF = 16 * ROW + 16 * 2 * 4;       // per warp: 16 rows + (mean, rstd) x 16
-  static constexpr int SMEM = NT * 32 * 8 + HID * 4 + WARPS * WBUF;  // B fragments, bias, per-warp buffers
+  static constexpr int NSEG = HID / 192;
+  static constexpr int TROW = NSEG * 416;                     // staged row (bytes)
+  static constexpr int WARPS = HID <= 384 ? 5 : 2;            // per CTA (2 CTAs per SM at hidden 384)
+  static constexpr int WBUF = 16 * TROW + 16 * 2 * 4;         // per warp: 16 rows + (mean, rstd) x 16
+  static constexpr int POS = 16 * HID * 4;                    // the CTA's pos (+ bias) slice, fp32
+  static constexpr int SMEM = NT * 32 * 8 + POS + WARPS * WBUF;
+  static_assert((TROW % 128) == 64, "staged rows must alternate 64-byte bank halves");
 };
+
+template <int HID>
+__device__ __forceinline__ int patch_seg_off(int col) {  // byte offset of hidden column col in a staged row
+  return (col / 192) * 416 + (col % 192) * 2;
+}
 
 template <int HID>
 __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_kernel(
     const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
     const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
-    float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
+    float ln_eps, const __grid_constant__ CUtensorMap tmRes, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
   using PM = PatchMma<HID>;
-  constexpr int NT = PM::NT, ROW = PM::ROW;
-  extern __shared__ __align__(16) uint8_t psm[];
+  constexpr int NT = PM::NT, TROW = PM::TROW;
+  extern __shared__ __align__(128) uint8_t psm[];
   uint2* sB = reinterpret_cast<uint2*>(psm);  // [NT][32 lanes]
+  float* sPos = reinterpret_cast<float*>(psm + NT * 32 * 8);  // [16][HID]: bias + pos of this CTA's tokens
   const uint32_t* pw32 = reinterpret_cast<const uint32_t*>(pw);  // [HID][8] bf16 pairs
-  float* sBias = reinterpret_cast<float*>(psm + NT * 32 * 8);
+  const int gw = HW / P, T = gw * gw, TG = T / 16;
+  const int tg = blockIdx.x % TG, tau0 = tg * 16;
   for (int idx = threadIdx.x; idx < NT * 32; idx += blockDim.x) {
     const int tile = idx / 32, gg = (idx % 32) / 4, cc = idx % 4;
     const int n = 32 * (tile / 4) + 8 * (gg >> 1) + 2 * (tile % 4) + (gg & 1);  // permuted weight row
     sB[idx] = make_uint2(pw32[n * 8 + cc], pw32[n * 8 + 4 + cc]);
   }
-  for (int idx = threadIdx.x; idx < HID; idx += blockDim.x) sBias[idx] = pb[idx];
+  for (int idx = threadIdx.x; idx < 16 * HID / 4; idx += blockDim.x) {
+    const int r = idx / (HID / 4), c4 = idx % (HID / 4);
+    const float4 pv = __ldg(reinterpret_cast<const float4*>(pos + (int64_t)(tau0 + r) * HID) + c4);
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(pb) + c4);
+    reinterpret_cast<float4*>(sPos)[idx] = make_float4(bv.x + pv.x, bv.y + pv.y, bv.z + pv.z, bv.w + pv.w);
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
-  uint8_t* sY = psm + NT * 32 * 8 + HID * 4 + warp * PM::WBUF;  // [16][ROW] staged bf16 residual rows
-  float* sStat = reinterpret_cast<float*>(sY + 16 * ROW);      // [16][mean, rstd]
-  const int gw = HW / P, T = gw * gw;
-  const int64_t groups = total_tokens / 16;
-  const int64_t wstride = (int64_t)gridDim.x * PM::WARPS;
-  for (int64_t grp = (int64_t)blockIdx.x * PM::WARPS + warp; grp < groups; grp += wstride) {
-    const int64_t tok0 = grp * 16;
-    const int64_t ni = tok0 / T;
-    const int tau0 = (int)(tok0 % T);
+  uint8_t* sY = psm + NT * 32 * 8 + PM::POS + warp * PM::WBUF;  // [16][TROW] staged bf16 residual rows
+  float* sStat = reinterpret_cast<float*>(sY + 16 * TROW);      // [16][rstd, -mean * rstd]
+  const int64_t rows = total_tokens / T;
+  const int64_t rstride = (int64_t)(gridDim.x / TG) * PM::WARPS;
+  const float* pos0 = sPos + g * HID + 8 * c;
+  const float* pos1 = pos0 + 8 * HID;
+  uint8_t* y0 = sY + g * TROW + 16 * c;
+  uint8_t* y1 = y0 + 8 * TROW;
+  // x of this lane for latent row ni: (row g, k 2c) (row g+8, k 2c) (row g, k 2c+8) (row g+8, k 2c+8)
+  auto load_x = [&](int64_t ni, float2 (&v)[4]) {
     const float* xl = x + (ni % lat_rows) * (int64_t)C * HW * HW;
-    uint32_t ahi[4], alo[4];  // A registers: (row g, k 2c) (row g+8, k 2c) (row g, k 2c+8) (row g+8, k 2c+8)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int tau = tau0 + g + 8 * (i & 1);
       const int pi = tau / gw, pj = tau % gw;
       const int ch = (c >> 1) + 2 * (i >> 1), p = c & 1;
-      const float2 v = __ldg(reinterpret_cast<const float2*>(xl + (int64_t)ch * HW * HW + (pi * 2 + p) * HW + pj * 2));
-      ahi[i] = pack_bf16(v.x, v.y);
-      const float2 h = unpack_bf16(ahi[i]);
-      alo[i] = pack_bf16(v.x - h.x, v.y - h.y);
+      v[i] = __ldg(reinterpret_cast<const float2*>(xl + (int64_t)ch * HW * HW + (pi * 2 + p) * HW + pj * 2));
     }
-    const float* pos0 = pos + (int64_t)(tau0 + g) * HID + 8 * c;
-    const float* pos1 = pos0 + 8 * HID;
-    uint8_t* y0 = sY + g * ROW + 16 * c;
-    uint8_t* y1 = y0 + 8 * ROW;
-    float sum0 = 0.f, sum1 = 0.f, sq0 = 0.f, sq1 = 0.f;
+  };
+  int64_t ni = (int64_t)(blockIdx.x / TG) * PM::WARPS + warp;
+  float2 xv[4];
+  if (ni < rows) load_x(ni, xv);
+  constexpr int J = HID / 128;
+  for (; ni < rows; ni += rstride) {
+    // (the bulk wait comes before the next row's x loads: it compiles to a scoreboard wait that
+    // would otherwise also wait for those loads)
+    if (lane == 0) bulk_wait_read<0>();  // the previous row's residual store has left sY
+    __syncwarp();
+    uint32_t ahi[4], alo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ahi[i] = pack_bf16(xv[i].x, xv[i].y);
+      const float2 h = unpack_bf16(ahi[i]);
+      alo[i] = pack_bf16(xv[i].x - h.x, xv[i].y - h.y);
+    }
+    if (ni + rstride < rows) load_x(ni + rstride, xv);  // next row's x in flight during this one
+    // this row's shift / scale for the copy-out (lane columns 4k, k = lane + 32j), also in flight
+    const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
+    const float* scale = shift + HID;
+    float4 sh[J], sc[J];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+      sh[jj] = __ldg(reinterpret_cast<const float4*>(shift + 4 * (lane + 32 * jj)));
+      sc[jj] = __ldg(reinterpret_cast<const float4*>(scale + 4 * (lane + 32 * jj)));
+    }
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {  // 1 + scale, once per row
+      sc[jj].x += 1.0f;
+      sc[jj].y += 1.0f;
+      sc[jj].z += 1.0f;
+      sc[jj].w += 1.0f;
+    }
+    const int64_t tok0 = ni * T + tau0;
+    // row statistics of the stored bf16 values in packed f32x2 (even / odd columns), as the block tail
+    float2 sum0 = make_float2(0.f, 0.f), sum1 = sum0, sq0 = sum0, sq1 = sum0;
 #pragma unroll 2
     for (int blk = 0; blk < HID / 32; ++blk) {
       float acc[4][4];
@@ -301,73 +349,72 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
         mma_bf16_16816(acc[q], alo[0], alo[1], alo[2], alo[3], b.x, b.y);
       }
       // lane columns 32 blk + 8c + {0..7}: column 2q + e <- acc[q][e] (row g), acc[q][2 + e] (row g+8)
-      float pb0[8], pb1[8], bias[8];
-      *reinterpret_cast<float4*>(&pb0[0]) = __ldg(reinterpret_cast<const float4*>(pos0 + 32 * blk));
-      *reinterpret_cast<float4*>(&pb0[4]) = __ldg(reinterpret_cast<const float4*>(pos0 + 32 * blk + 4));
-      *reinterpret_cast<float4*>(&pb1[0]) = __ldg(reinterpret_cast<const float4*>(pos1 + 32 * blk));
-      *reinterpret_cast<float4*>(&pb1[4]) = __ldg(reinterpret_cast<const float4*>(pos1 + 32 * blk + 4));
-      *reinterpret_cast<float4*>(&bias[0]) = *reinterpret_cast<const float4*>(sBias + 32 * blk + 8 * c);
-      *reinterpret_cast<float4*>(&bias[4]) = *reinterpret_cast<const float4*>(sBias + 32 * blk + 8 * c + 4);
+      float pb0[8], pb1[8];
+      *reinterpret_cast<float4*>(&pb0[0]) = *reinterpret_cast<const float4*>(pos0 + 32 * blk);
+      *reinterpret_cast<float4*>(&pb0[4]) = *reinterpret_cast<const float4*>(pos0 + 32 * blk + 4);
+      *reinterpret_cast<float4*>(&pb1[0]) = *reinterpret_cast<const float4*>(pos1 + 32 * blk);
+      *reinterpret_cast<float4*>(&pb1[4]) = *reinterpret_cast<const float4*>(pos1 + 32 * blk + 4);
       uint32_t r0[4], r1[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // residual, stored bf16 (bias + pos first, as the FMA kernel)
-        r0[q] = pack_bf16(acc[q][0] + (bias[2 * q] + pb0[2 * q]), acc[q][1] + (bias[2 * q + 1] + pb0[2 * q + 1]));
-        r1[q] = pack_bf16(acc[q][2] + (bias[2 * q] + pb1[2 * q]), acc[q][3] + (bias[2 * q + 1] + pb1[2 * q + 1]));
+      for (int q = 0; q < 4; ++q) {  // residual, stored bf16 (bias + pos first)
+        const float2 v0 = __fadd2_rn(make_float2(acc[q][0], acc[q][1]), make_float2(pb0[2 * q], pb0[2 * q + 1]));
+        const float2 v1 = __fadd2_rn(make_float2(acc[q][2], acc[q][3]), make_float2(pb1[2 * q], pb1[2 * q + 1]));
+        r0[q] = pack_bf16(v0.x, v0.y);
+        r1[q] = pack_bf16(v1.x, v1.y);
         const float2 f0 = unpack_bf16(r0[q]), f1 = unpack_bf16(r1[q]);
-        sum0 += f0.x + f0.y;
-        sum1 += f1.x + f1.y;
-        sq0 += f0.x * f0.x + f0.y * f0.y;
-        sq1 += f1.x * f1.x + f1.y * f1.y;
+        sum0 = __fadd2_rn(sum0, f0);
+        sum1 = __fadd2_rn(sum1, f1);
+        sq0 = __ffma2_rn(f0, f0, sq0);
+        sq1 = __ffma2_rn(f1, f1, sq1);
       }
-      *reinterpret_cast<uint4*>(y0 + 64 * blk) = make_uint4(r0[0], r0[1], r0[2], r0[3]);
-      *reinterpret_cast<uint4*>(y1 + 64 * blk) = make_uint4(r1[0], r1[1], r1[2], r1[3]);
+      const int off = (blk / 6) * 416 + (blk % 6) * 64;
+      *reinterpret_cast<uint4*>(y0 + off) = make_uint4(r0[0], r0[1], r0[2], r0[3]);
+      *reinterpret_cast<uint4*>(y1 + off) = make_uint4(r1[0], r1[1], r1[2], r1[3]);
     }
+    float s0 = sum0.x + sum0.y, s1 = sum1.x + sum1.y, q0 = sq0.x + sq0.y, q1 = sq1.x + sq1.y;
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
-      sum0 += __shfl_xor_sync(0xffffffffu, sum0, o);
-      sum1 += __shfl_xor_sync(0xffffffffu, sum1, o);
-      sq0 += __shfl_xor_sync(0xffffffffu, sq0, o);
-      sq1 += __shfl_xor_sync(0xffffffffu, sq1, o);
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+      q1 += __shfl_xor_sync(0xffffffffu, q1, o);
     }
-    if (c == 0) {
-      const float mean0 = sum0 / HID, mean1 = sum1 / HID;
-      sStat[2 * g] = mean0;
-      sStat[2 * g + 1] = rsqrtf(fmaxf(sq0 / HID - mean0 * mean0, 0.f) + ln_eps);
-      sStat[2 * (g + 8)] = mean1;
-      sStat[2 * (g + 8) + 1] = rsqrtf(fmaxf(sq1 / HID - mean1 * mean1, 0.f) + ln_eps);
+    if (c == 0) {  // per row: rstd and -mean * rstd (LN(x) = x * rstd - mean * rstd)
+      const float mean0 = s0 / HID, mean1 = s1 / HID;
+      const float rs0 = rsqrtf(fmaxf(q0 / HID - mean0 * mean0, 0.f) + ln_eps);
+      const float rs1 = rsqrtf(fmaxf(q1 / HID - mean1 * mean1, 0.f) + ln_eps);
+      sStat[2 * g] = rs0;
+      sStat[2 * g + 1] = -mean0 * rs0;
+      sStat[2 * (g + 8)] = rs1;
+      sStat[2 * (g + 8) + 1] = -mean1 * rs1;
     }
+    fence_proxy_async_smem();  // the staged residual is read by the TMA store (async proxy)
     __syncwarp();
-    // copy-out: 8 B (4 columns) per lane and row, each lane on fixed columns 4k, k = lane + 32j, so the
-    // slot's shift/scale for them are loaded once per group; LN + modulate on the staged bf16 residual
-    const float* shift = mod + ni * mod_stride;  // block 0: shift_msa at 0, scale_msa at HID
-    const float* scale = shift + HID;
-    constexpr int J = HID / 128;
-    float4 sh[J], sc[J];
-#pragma unroll
-    for (int jj = 0; jj < J; ++jj) {
-      sh[jj] = __ldg(reinterpret_cast<const float4*>(shift + 4 * (lane + 32 * jj)));
-      sc[jj] = __ldg(reinterpret_cast<const float4*>(scale + 4 * (lane + 32 * jj)));
+    if (lane == 0) {
+      tma_store_2d(&tmRes, sY, 0, (int)(tok0 * PM::NSEG));
+      bulk_commit();
     }
+    // copy-out of LN + modulate: 8 B (4 columns) per lane and row, each lane on fixed columns 4k
 #pragma unroll 2
     for (int row = 0; row < 16; ++row) {
-      const float mean = sStat[2 * row], rstd = sStat[2 * row + 1];
+      const float2 r2 = make_float2(sStat[2 * row], sStat[2 * row]);
+      const float2 c2 = make_float2(sStat[2 * row + 1], sStat[2 * row + 1]);
 #pragma unroll
       for (int jj = 0; jj < J; ++jj) {
         const int k = lane + 32 * jj;
-        const uint2 v = *reinterpret_cast<const uint2*>(sY + row * ROW + 8 * k);
-        const int64_t off = (tok0 + row) * HID + 4 * k;
-        *reinterpret_cast<uint2*>(xres + off) = v;
-        const float2 a = unpack_bf16(v.x), b = unpack_bf16(v.y);
-        uint2 o;
-        o.x = pack_bf16((a.x - mean) * rstd * (1.0f + sc[jj].x) + sh[jj].x,
-                        (a.y - mean) * rstd * (1.0f + sc[jj].y) + sh[jj].y);
-        o.y = pack_bf16((b.x - mean) * rstd * (1.0f + sc[jj].z) + sh[jj].z,
-                        (b.y - mean) * rstd * (1.0f + sc[jj].w) + sh[jj].w);
-        *reinterpret_cast<uint2*>(xmod + off) = o;
+        const uint2 v = *reinterpret_cast<const uint2*>(sY + row * TROW + patch_seg_off<HID>(4 * k));
+        // LN(x) * (1 + scale) + shift in packed f32x2, the block tail's epilogue form
+        const float2 ya = __ffma2_rn(__ffma2_rn(unpack_bf16(v.x), r2, c2), make_float2(sc[jj].x, sc[jj].y),
+                                     make_float2(sh[jj].x, sh[jj].y));
+        const float2 yb = __ffma2_rn(__ffma2_rn(unpack_bf16(v.y), r2, c2), make_float2(sc[jj].z, sc[jj].w),
+                                     make_float2(sh[jj].z, sh[jj].w));
+        *reinterpret_cast<uint2*>(xmod + (tok0 + row) * HID + 4 * k) =
+            make_uint2(pack_bf16(ya.x, ya.y), pack_bf16(yb.x, yb.y));
       }
     }
-    __syncwarp();  // staged rows consumed before the next group overwrites them
+    __syncwarp();  // staged rows / stats consumed before the next row overwrites them
   }
+  if (lane == 0) bulk_wait<0>();
 }
 
 // ============================================================ K4: LayerNorm + adaLN modulate (wide rows)
@@ -698,6 +745,7 @@ struct sf_dit {
   std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
   AttnMaps attn_maps;
   CUtensorMap fin_x, fin_w;  // final layer: xmod / final weight rows as 208-wide segment boxes
+  CUtensorMap pe_res;        // patch embed: xres as 208-wide segment boxes (TMA store)
   // One instantiated graph per distinct argument set of sf_dit_stream_step: every pointer and
   // value the capture bakes into a launch is part of the key, so a replay is always the launch
   // sequence an eager call with the same arguments would enqueue.  Owners release their graphs
@@ -865,12 +913,16 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   const int64_t tokens = rows * h->tokens;
   const size_t sm = c.hidden == 384 ? PatchMma<384>::SMEM : PatchMma<1152>::SMEM;
   const int wpb = c.hidden == 384 ? PatchMma<384>::WARPS : PatchMma<1152>::WARPS;
-  // persistent: as many CTAs as fit (smem-limited: 2 per SM at hidden 384, 1 at 1152), each warp
-  // walks several 16-token groups, so the B-fragment fill is paid once per CTA
-  const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, c.hidden == 384 ? 2 * 148 : 148);
+  // CTA c: token group c % TG of latent rows c / TG + k * (CTAs / TG); as many row blocks per
+  // group as fill the resident CTA slots (smem-limited: 2 per SM at hidden 384, 1 at 1152)
+  const int TG = h->tokens / 16;
+  const int64_t slots = c.hidden == 384 ? 2 * 148 : 148;
+  int64_t per = std::max<int64_t>(1, slots / TG);
+  per = std::min<int64_t>(per, (rows + wpb - 1) / wpb);
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
-  kern<<<blocks, 32 * wpb, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch, (const __nv_bfloat16*)h->w.patch_w,
-                                h->w.patch_b, h->w.pos_embed, h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens);
+  kern<<<(unsigned)(TG * per), 32 * wpb, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch,
+                                                   (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b, h->w.pos_embed,
+                                                   h->mod, h->mod_stride, c.ln_eps, h->pe_res, h->xmod, tokens);
   mark(h, P_PATCH, st);
   return cuda_status();
 }
@@ -959,6 +1011,9 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     }
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens, c.hidden / c.heads);
+  // [rows, HID] -> [rows * HID/192, 192], 208-wide boxes of 16 rows' segments (same view as the final layer)
+  rc |= make_tmap_bf16_2d(&h->pe_res, h->xres, 192, (uint64_t)max_rows * h->tokens * (c.hidden / 192), 192, 208,
+                          16 * (c.hidden / 192), 0);
   if (c.hidden == 384) {
     rc |= make_final_map<384>(&h->fin_x, h->xmod, max_rows * h->tokens);
     rc |= make_final_map<384>(&h->fin_w, w->final_w, 16);
