@@ -163,6 +163,7 @@ def run_mock(args):
         return total, [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
 
     clocks = Clocks(local)
+    clocks.start()
     total_ms, step_ms = timed(sb.launch, args.steps)
     clk = clocks.stop()
     frames = world * S * args.steps
@@ -266,47 +267,67 @@ def workload(args, world):
 
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler (every 20 ms) around a timed region: `Clocks(gpu)` starts it and waits
+    for its first sample, `start()` / `stop()` bracket the timed region; only samples stamped
+    inside the region count (the first one after it starts when the region is shorter than the
+    sampling interval)."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.path = tempfile.mktemp(suffix=".csv")
         self.proc = None
+        self.t0 = self.t1 = None
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            deadline = time.time() + 5.0
+            while time.time() < deadline and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
+    def start(self):
+        self.t0 = time.time()
+
     def stop(self) -> dict:
+        import datetime
+
+        self.t1 = time.time()
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)  # the sample that follows the region's end
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         self.fh.close()
-        sm, mx, reasons = [], None, set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             p = [x.strip() for x in line.split(",")]
-            if len(p) < 9:
+            if len(p) < 10:
                 continue
             try:
-                sm.append(float(p[1]))
-                mx = float(p[2])
+                ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(p[2]), float(p[3]), {nm for nm, v in zip(names, p[6:10])
+                                                             if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
         os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
-                "reasons": sorted(reasons)}
+        t0 = self.t0 if self.t0 is not None else -1e18
+        inside = [r for r in rows if t0 <= r[0] <= self.t1]
+        if not inside:  # region shorter than the sampling interval: the first sample after its start
+            after = [r for r in rows if r[0] >= t0]
+            inside = after[:1]
+        sm = [r[1] for r in inside]
+        reasons = set().union(*[r[3] for r in inside]) if inside else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": inside[-1][2] if inside else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
 
 
 def peaks():
@@ -428,6 +449,7 @@ def main():
 
     clocks = Clocks(local)
     j0 = sb.j
+    clocks.start()
     total_ms, step_ms = timed(sb.launch, args.steps)
     clk = clocks.stop()
     # output guard: the last timed step retired generation j-n+1 of every stream, finite
