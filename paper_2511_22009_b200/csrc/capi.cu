@@ -20,8 +20,9 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % 128) return SF_ERR_PARAMETER;
   if (epi < EPI_F32 || epi > EPI_GELU) return SF_ERR_PARAMETER;
   const int bn = (N % 256 == 0) ? 256 : 128;
+  const int ctas = (epi == EPI_GELU && bn == 256) ? 2 : 1;  // 256-row pair tiles, as the DiT-XL/2 fc1
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, bn) != SF_OK) return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn, ctas) != SF_OK) return SF_ERR_CUDA;
   if (epi != EPI_F32 && (gemm_narrow_out(bn, epi) ? make_out_map32(&maps.d[0], C, M, N)
                                                   : make_out_map(&maps.d[0], C, M, N)) != SF_OK)
     return SF_ERR_CUDA;
@@ -31,7 +32,7 @@ int sf_gemm_bf16(const void* A, const void* W, const float* bias, void* C, int64
   ep.ldo = N;
   ep.tokens_per_slot = 1 << 30;
   ep.M = (int)M;
-  return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(epi, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream, ctas);
 }
 
 int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, void* k, void* vt, int64_t M,
@@ -39,7 +40,7 @@ int sf_gemm_qkv_hd(const void* A, const void* W, const float* bias, void* q, voi
   const int bn = hd == 64 ? qkv_bn64() : 144;
   const int64_t d = (int64_t)heads * hd, N = 3 * d, K = d;
   if ((hd != 64 && hd != 72) || M < 1 || T < 128 || M % T || T % 128 || N % bn || K % 64) return SF_ERR_PARAMETER;
-  const int ctas = hd == 64 ? qkv_ctas(K) : 1;
+  const int ctas = hd == 64 ? qkv_ctas(K) : 2;  // the runtime's configurations (dit_runtime.cu run_blocks)
   GemmMaps maps;
   if (make_operand_maps(&maps, A, M, K, W, N, bn, ctas) != SF_OK) return SF_ERR_CUDA;
   if (make_qkv_out_maps(&maps, q, k, vt, M / T, heads, T, hd) != SF_OK) return SF_ERR_CUDA;
@@ -61,8 +62,10 @@ int sf_gemm_res(const void* A, const void* W, const float* bias, void* xres, con
                 int64_t M, int64_t N, int64_t K, int32_t tokens_per_slot, void* stream) {
   if (N % 128 || K % 64 || M < 1 || tokens_per_slot < 128 || M % tokens_per_slot || tokens_per_slot % 128)
     return SF_ERR_PARAMETER;
+  // N % 192 == 0: 256 x 192 pair tiles (the DiT-XL/2 proj / fc2 configuration), else 128 x 128
+  const int bn = N % 192 == 0 ? 192 : 128, ctas = bn == 192 ? 2 : 1;
   GemmMaps maps;
-  if (make_operand_maps(&maps, A, M, K, W, N, 128) != SF_OK) return SF_ERR_CUDA;
+  if (make_operand_maps(&maps, A, M, K, W, N, bn, ctas) != SF_OK) return SF_ERR_CUDA;
   if (make_out_map(&maps.d[0], xres, M, N) != SF_OK) return SF_ERR_CUDA;
   EpiParams ep{};
   ep.bias = bias;
@@ -70,7 +73,7 @@ int sf_gemm_res(const void* A, const void* W, const float* bias, void* xres, con
   ep.vec_stride = vec_stride;
   ep.tokens_per_slot = tokens_per_slot;
   ep.M = (int)M;
-  return launch_gemm(EPI_RES, 128, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream);
+  return launch_gemm(EPI_RES, bn, maps, (int)M, (int)N, (int)K, ep, (cudaStream_t)stream, ctas);
 }
 
 int sf_ln_modulate(const void* xres, void* xmod, const float* shift, const float* scale, int64_t vec_stride,

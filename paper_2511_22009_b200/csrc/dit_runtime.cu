@@ -838,7 +838,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.tokens_per_slot = T;
       ep.M = (int)M;
       if ((rc = launch_gemm(EPI_QKV, hd == 64 ? qkv_bn64() : 144, h->g_qkv[l], (int)M, 3 * H, H, ep, st,
-                            hd == 64 ? qkv_ctas(H) : 1)))
+                            hd == 64 ? qkv_ctas(H) : 2)))
         return rc;
       mark(h, P_QKV, st);
     }
@@ -862,8 +862,8 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       mark(h, P_TAIL, st);
       continue;
     }
-    // DiT-XL/2 (1152-wide rows): gated-residual GEMM epilogues (128-wide tiles) + a LayerNorm /
-    // modulate pass, with fc1 + GELU in between
+    // DiT-XL/2 (1152-wide rows): gated-residual GEMM epilogues + a LayerNorm / modulate pass, with
+    // fc1 + GELU in between; every GEMM on 256-row CTA-pair tiles (B split across the pair)
     for (int half = 0; half < 2; ++half) {  // 0: attention proj (gate_msa), 1: MLP (fc1 + GELU, fc2, gate_mlp)
       if (half == 1) {
         EpiParams ep{};
@@ -871,7 +871,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
         ep.ldo = c.mlp_hidden;
         ep.tokens_per_slot = T;
         ep.M = (int)M;
-        if ((rc = launch_gemm(EPI_GELU, 256, h->g_fc1[l], (int)M, c.mlp_hidden, H, ep, st))) return rc;
+        if ((rc = launch_gemm(EPI_GELU, 256, h->g_fc1[l], (int)M, c.mlp_hidden, H, ep, st, 2))) return rc;
         mark(h, P_FC1, st);
       }
       const GemmMaps& gm = half == 0 ? h->g_proj[l] : h->g_fc2[l];
@@ -884,7 +884,7 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
       ep.vec_stride = h->mod_stride;
       ep.tokens_per_slot = T;
       ep.M = (int)M;
-      if ((rc = launch_gemm(EPI_RES, 128, gm, (int)M, H, K, ep, st))) return rc;
+      if ((rc = launch_gemm(EPI_RES, 192, gm, (int)M, H, K, ep, st, 2))) return rc;
       mark(h, cls, st);
       const float* ln = half == 0 ? mb + 3 * H : nxt;  // the MLP's (shift_mlp, scale_mlp) / what follows
       if ((rc = launch_ln_modulate(h->xres, h->xmod, ln, ln + H, h->mod_stride, M, H, T, c.ln_eps, st))) return rc;
@@ -999,14 +999,14 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     const __nv_bfloat16* fc2 = (const __nv_bfloat16*)w->fc2_w + (int64_t)l * H * c.mlp_hidden;
     const int hd = H / c.heads;
     rc |= make_operand_maps(&h->g_qkv[l], h->xmod, M, H, qkv, 3 * H, hd == 64 ? qkv_bn64() : 144,
-                            hd == 64 ? qkv_ctas(H) : 1);
+                            hd == 64 ? qkv_ctas(H) : 2);
     rc |= make_qkv_out_maps(&h->g_qkv[l], h->q, h->k, h->vt, max_rows, c.heads, h->tokens, hd);
     if (H != 384) {  // DiT-XL/2 MLP + projection as GEMMs: RES epilogue (128-wide tiles) + LayerNorm pass
-      rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256);
+      rc |= make_operand_maps(&h->g_fc1[l], h->xmod, M, H, fc1, c.mlp_hidden, 256, 2);
       rc |= make_out_map32(&h->g_fc1[l].d[0], h->hmid, M, c.mlp_hidden);  // 256-wide GELU tiles: 32-column chunks
-      rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 128);
+      rc |= make_operand_maps(&h->g_proj[l], h->attn, M, H, proj, H, 192, 2);
       rc |= make_out_map(&h->g_proj[l].d[0], h->xres, M, H);
-      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 128);
+      rc |= make_operand_maps(&h->g_fc2[l], h->hmid, M, c.mlp_hidden, fc2, H, 192, 2);
       rc |= make_out_map(&h->g_fc2[l].d[0], h->xres, M, H);
     }
   }

@@ -95,9 +95,12 @@ int qkv_ctas(int64_t K) { return K == 64 * GemmCfg<192, 8, EPI_QKV, 2>::KB_RES ?
 template <int BN, int KIND, int CTAS = 1>
 constexpr int epi_warps() {
   // QKV: 4 (pair tiles: 8 = two groups of 4 draining alternate tiles); RES_LN: 12;
-  // bf16 / GELU with 256-wide tiles: 16 (4 per TMEM lane quarter); else 8
+  // RES with 192-wide tiles: 12 (64 columns per thread); bf16 / GELU with 256-wide tiles:
+  // 16 (4 per TMEM lane quarter); else 8
   return KIND == EPI_QKV ? (BN == 192 ? (CTAS == 2 ? 8 : 4) : BN == 128 ? 8 : 4)
-                         : KIND == EPI_RES_LN ? 12 : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
+         : KIND == EPI_RES_LN ? 12
+         : (KIND == EPI_RES && BN == 192) ? 12
+         : ((KIND == EPI_BF16 || KIND == EPI_GELU) && BN == 256) ? 16 : 8;
 }
 
 // Whether the epilogue of (BN, KIND) stages 32-column chunks (output map: make_out_map32).
@@ -135,6 +138,9 @@ int prepare_gemm_kernels() {
   rc |= set_attr<256, EPI_GELU>();
   rc |= set_attr<192, EPI_QKV>();
   rc |= set_attr<192, EPI_QKV, 2>();
+  rc |= set_attr<144, EPI_QKV, 2>();
+  rc |= set_attr<256, EPI_GELU, 2>();
+  rc |= set_attr<192, EPI_RES, 2>();
   rc |= set_attr<128, EPI_QKV>();
   rc |= set_attr<384, EPI_RES_LN>();
   rc |= set_attr<144, EPI_QKV>();
@@ -168,12 +174,13 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
   e.M = M;
   cudaError_t err;
   if constexpr (CTAS == 2) {
-    // pairs: a multiple of N / BN so every pair keeps one column slice (B resident)
     const int num_n = N / BN, pair_tiles = num_n * ((M + 2 * C::BM - 1) / (2 * C::BM));
     int pairs = sm_count() / 2;
     if (pairs > pair_tiles) pairs = pair_tiles;
-    pairs -= pairs % num_n;
-    if (pairs < num_n) pairs = num_n;
+    if (C::B_RES) {  // a multiple of N / BN pairs, so every pair keeps one column slice
+      pairs -= pairs % num_n;
+      if (pairs < num_n) pairs = num_n;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * pairs));
     cfg.blockDim = dim3(C::THREADS);
@@ -225,6 +232,9 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
   if (K % 32 != 0 || N % bn != 0 || M <= 0) return SF_ERR_PARAMETER;
   if (ctas == 2) {
     if (bn == 192 && kind == EPI_QKV) return launch_one<192, EPI_QKV, 2>(maps, M, N, K, ep, st);
+    if (bn == 144 && kind == EPI_QKV) return launch_one<144, EPI_QKV, 2>(maps, M, N, K, ep, st);
+    if (bn == 256 && kind == EPI_GELU) return launch_one<256, EPI_GELU, 2>(maps, M, N, K, ep, st);
+    if (bn == 192 && kind == EPI_RES) return launch_one<192, EPI_RES, 2>(maps, M, N, K, ep, st);
     return SF_ERR_PARAMETER;
   }
 #define SF_CASE(BN_, KIND_) \

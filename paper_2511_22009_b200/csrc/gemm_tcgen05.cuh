@@ -82,12 +82,14 @@ struct GemmCfg {
   static constexpr int SWZ = BK * 2;             // swizzle width of the operand tiles (bytes)
   static constexpr int A_BYTES = BM * BK * 2;
   // CTAS = 2: a cluster pair computes 256 x BN tiles with cta_group::2 MMAs; each CTA
-  // holds its 128 A rows and BN/2 B rows (the pair MMA reads B from both).  The pair keeps
-  // one column slice n for its whole life and its half of that B slice stays RESIDENT in
-  // smem (K = KB_RES * BK), so only A streams through the ring: per 128 x BN tile a CTA
-  // pulls 96 KB of A from L2 instead of 96 KB of A + 144 KB of B (the single-CTA QKV GEMM
-  // waits on its operand ring, not on the tensor pipe or the epilogue: ncu, profiles/r02).
-  static constexpr bool B_RES = CTAS == 2;
+  // holds its 128 A rows and BN/2 B rows (the pair MMA reads B from both), so per 128-row
+  // tile a CTA pulls half the B bytes from L2 (the DiT-XL/2 GEMMs, K = 1152 / 4608: their
+  // single-CTA tiles are fed at ~64-85 FLOP per L2 byte).  For the DiT-S/2 QKV (K = 384,
+  // BN = 192) the pair keeps one column slice n for its whole life and its half of that B
+  // slice stays RESIDENT in smem (K = KB_RES * BK), so only A streams through the ring: per
+  // 128 x BN tile a CTA pulls 96 KB of A from L2 instead of 96 KB of A + 144 KB of B (the
+  // single-CTA QKV GEMM waits on its operand ring, not on the tensor pipe: profiles/r02).
+  static constexpr bool B_RES = CTAS == 2 && KIND == EPI_QKV && BN == 192;
   static constexpr int KB_RES = 6;  // resident K blocks (K = 384, the DiT-S/2 hidden size)
   static constexpr int B_ROWS = BN / CTAS;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
