@@ -100,3 +100,28 @@ def test_gemm_qkv_hd72_and_res_ln_pass():
     ln = torch.nn.functional.layer_norm(xres.float(), (D,), eps=1e-6)
     want = ln * (1 + vec[slot, 2 * D:]) + vec[slot, D:2 * D]
     assert (xmod.float() - want).abs().max().item() < 3e-2 * max(1.0, want.abs().max().item())
+
+
+@pytest.mark.parametrize("M,K,T", [(1152, 1152, 128), (384, 4608, 128), (2048, 4608, 1024)])
+def test_gemm_res_pair_tiles_ragged(M, K, T):
+    """sf_gemm_res at N = 1152 runs on 256 x 192 CTA-pair tiles (the DiT-XL/2 proj / fc2 path): an
+    odd number of 128-row tiles leaves the second CTA of the last pair past M (loads zero-filled,
+    stores masked); K = 4608 is the fc2 depth.  Rows past M must stay untouched."""
+    from paper_2511_22009_b200 import _lib
+
+    st = torch.cuda.current_stream().cuda_stream
+    D = 1152
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(D, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    b = torch.randn(D, device="cuda", generator=g) * 0.1
+    x0 = torch.randn(M + 128, D, device="cuda", generator=g).to(torch.bfloat16)  # + a guard block
+    xres = x0.clone()
+    vec = torch.randn(M // T, D, device="cuda", generator=g) * 0.5
+    _lib.call("sf_gemm_res", a.data_ptr(), w.data_ptr(), b.data_ptr(), xres.data_ptr(), vec.data_ptr(), D,
+              M, D, K, T, st)
+    torch.cuda.synchronize()
+    slot = torch.arange(M, device="cuda") // T
+    ref = x0[:M].float() + vec[slot] * (a.float() @ w.float().t() + b)
+    assert (xres[:M].float() - ref).abs().max().item() < 3e-2 * max(1.0, ref.abs().max().item())
+    assert torch.equal(xres[M:], x0[M:])

@@ -12,19 +12,20 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_22009_b200 as sf  # noqa: E402
-from paper_2511_22009_b200.dit import DIT_S2  # noqa: E402
+from paper_2511_22009_b200.dit import DIT_S2, DIT_XL2  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--streams", type=int, default=10)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--guidance", type=float, default=1.0)
+ap.add_argument("--xl", action="store_true", help="DiT-XL/2 stream step instead (pair-tile GEMMs, head dim 72)")
 a = ap.parse_args()
 n = 4
 sched = sf.build_time_window_schedule(inference_steps=n)
 mock = sf.SeededMockModel(dim=4096, seed=1)
 cond = sf.make_conditioning(np.ones(8), guidance_scale=a.guidance)
 res, _ = sf.run_stream(3, n, mock, cond, 5, sched)
-model = sf.DiTVelocityModel(DIT_S2, seed=0, max_rows=2 * a.streams * n)
+model = sf.DiTVelocityModel(DIT_XL2 if a.xl else DIT_S2, seed=0, max_rows=2 * a.streams * n)
 conds = [sf.make_conditioning(np.random.default_rng([s, 7]).standard_normal(8), guidance_scale=a.guidance)
          for s in range(a.streams)]
 sb = sf.StreamBatch(model, sched, n, num_streams=a.streams, cond=conds, seed=0, dtype=np.float32, noise="device",
