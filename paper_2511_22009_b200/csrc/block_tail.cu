@@ -50,7 +50,7 @@ constexpr int GCOLS = HC / PARTS;             // 32 hidden columns per worker th
 constexpr int THREADS = 32 * (2 + WORKERS);
 constexpr int ACC2 = 0, ACC1 = 384;
 constexpr uint16_t PAIR_MASK = 0x3;
-constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + H_BYTES + 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 512;
+constexpr int SMEM = 1024 + X_BYTES + NSTAGE * STAGE + H_BYTES + 2 * 4 * D * 4 + 2 * 4 * BM * 4 + FF * 4 + 512;
 static_assert(SMEM <= 232448, "shared memory");
 
 struct Params {
@@ -111,8 +111,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint8_t* sX = smem;
   uint8_t* sW = sX + X_BYTES;
   uint8_t* sH = sW + NSTAGE * STAGE;
-  float* sVec = reinterpret_cast<float*>(sH + H_BYTES);  // bias | gate | shift | scale  [4][384]
-  float* sRed = sVec + 4 * D;                            // [2 stats][PARTS][128 rows]
+  // per-column vectors of the two epilogues, [4][384] each (bias | gate | shift | scale): the
+  // projection epilogue's (sVecP) and the final epilogue's (sVecF), filled during the MLP phase of
+  // the tile before / the same tile so neither epilogue starts with global loads
+  float* sVecP = reinterpret_cast<float*>(sH + H_BYTES);
+  float* sVecF = sVecP + 4 * D;
+  float* sRed = sVecF + 4 * D;                           // [2 stats][PARTS][128 rows]
   float* sB1 = sRed + 2 * 4 * BM;                        // fc1 bias [1536]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB1 + FF);
   uint64_t* wfull = bars;               // [NSTAGE] (leader) both halves of a weight block landed
@@ -376,7 +380,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       named_bar_sync(2 + quarter, 32 * PARTS);  // the stores have read the quarter's rows
     };
     // per-column vectors of one epilogue, pre-combined: [gate * bias | gate | shift | 1 + scale]
-    auto load_vecs = [&](const float* bias, const float* gate, const float* shift, const float* scale, int64_t slot) {
+    // (called where every worker is past the previous readers of sVec: between two GELU chunks)
+    auto load_vecs = [&](float* sVec, const float* bias, const float* gate, const float* shift, const float* scale,
+                         int64_t slot) {
       named_bar_sync(1, WORKERS * 32);  // the previous readers are done with sVec
       for (int i = e * 32 + lane; i < D; i += WORKERS * 32) {
         const int64_t o = slot * p.vec_stride + i;
@@ -398,8 +404,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (e == 0 && lane == 0 && ep_mark + k < 64) g_trace[(8 * (blockIdx.x & 1) + 1) * 128 + 32 + ep_mark + k] = clock64();
 #endif
     };
-    auto res_ln = [&](int r0, uint64_t* acc_full, uint32_t acc_ph, uint64_t* rows_full, uint32_t rows_ph,
-                      auto done_acc) {
+    auto res_ln = [&](const float* sVec, int r0, uint64_t* acc_full, uint32_t acc_ph, uint64_t* rows_full,
+                      uint32_t rows_ph, auto done_acc) {
       mbar_wait(acc_full, acc_ph);
       mark(0);
       mbar_wait(rows_full, rows_ph);
@@ -477,14 +483,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mark(4);
     };
     int g = 0, local = 0;
+    if (pair0 < pairs) load_vecs(sVecP, p.bp, p.g1, p.sh1, p.sc1, (2 * pair0 + (int)crank) * BM / p.T);
     for (int pr = pair0; pr < pairs; pr += pstride, ++local) {
       const int r0 = (2 * pr + (int)crank) * BM;
       const int64_t slot = r0 / p.T;
       // ---- projection epilogue: x = xres + gate_msa * (acc + b_proj) -> xres; X <- LN_mlp(x)
-      load_vecs(p.bp, p.g1, p.sh1, p.sc1, slot);
       if (e == 0 && lane == 0) TTR(1, 4 * local);
       ep_mark = 16 * local;
-      res_ln(r0, pfull, local & 1, r1full, local & 1, [] {});
+      res_ln(sVecP, r0, pfull, local & 1, r1full, local & 1, [] {});
       fence_proxy_async_smem();  // h is read by the fc1 MMAs (async proxy)
       arrive_lead(xready);       // (all TMEM reads of the projection accumulator precede this)
       if (e == 0 && lane == 0) TTR(1, 4 * local + 1);
@@ -527,12 +533,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         fence_proxy_async_smem();
         arrive_lead(hfull);
+        // the two epilogues' vectors, between GELU chunks (off the epilogues' critical path)
+        if (c == 1) load_vecs(sVecF, p.b2, p.g2, p.sh2, p.sc2, slot);
+        if (c == 6 && pr + pstride < pairs)
+          load_vecs(sVecP, p.bp, p.g1, p.sh1, p.sc1, (2 * (pr + pstride) + (int)crank) * BM / p.T);
       }
       // ---- final epilogue: x' = x + gate_mlp * (acc + b2) -> xres; LN_next(x') -> xmod
-      load_vecs(p.b2, p.g2, p.sh2, p.sc2, slot);
       if (e == 0 && lane == 0) TTR(1, 4 * local + 2);
       ep_mark = 16 * local + 8;
-      res_ln(r0, a2full, local & 1, r2full, local & 1, [&] { arrive_lead(a2empty); });
+      res_ln(sVecF, r0, a2full, local & 1, r2full, local & 1, [&] { arrive_lead(a2empty); });
       store_quarter(&tmMs, r0);  // LN_next(x') out
       mark(5);
       arrive_local(xfree);
