@@ -142,7 +142,10 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       : "memory");
 }
 
-template <int HD>
+// PDL = launched with programmatic serialisation (small batches, sf_internal.h g_pdl): a separate
+// instantiation, because any PDL code in the kernel measured 2-5% slower at full occupancy through
+// the softmax's register allocation
+template <int HD, bool PDL>
 __global__ void __launch_bounds__(attn::THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQh,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKh,
@@ -216,6 +219,10 @@ __global__ void __launch_bounds__(attn::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if constexpr (PDL) {
+    if (threadIdx.x == 0) pdl_trigger(true);  // the next kernel's CTAs may start their prologue
+    pdl_wait(true);                           // Q / K / V^T of the previous kernel are complete
+  }
 
   if (warp == 8) {
     if (lane == 0) {
@@ -463,19 +470,34 @@ static int attn_sm_count() {
   return n;
 }
 
-template <int HD>
+template <int HD, bool PDL>
 static int prepare_attn_hd() {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_fwd_tcgen05<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<HD>::SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(attn_fwd_tcgen05<HD, PDL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             AttnCfg<HD>::SMEM) != cudaSuccess)
       return SF_ERR_CUDA;
     attr = true;
   }
   return SF_OK;
 }
 
-int prepare_attn_kernel() { return prepare_attn_hd<64>() == SF_OK && prepare_attn_hd<72>() == SF_OK ? SF_OK : SF_ERR_CUDA; }
+int prepare_attn_kernel() {
+  return prepare_attn_hd<64, false>() == SF_OK && prepare_attn_hd<72, false>() == SF_OK &&
+                 prepare_attn_hd<64, true>() == SF_OK && prepare_attn_hd<72, true>() == SF_OK
+             ? SF_OK
+             : SF_ERR_CUDA;
+}
+
+template <int HD>
+static cudaError_t launch_attn_hd(const AttnMaps& m, __nv_bfloat16* out, int T, int heads, int items, int grid,
+                                  cudaStream_t st) {
+  if (g_pdl)
+    return launch_kernel(attn_fwd_tcgen05<HD, true>, dim3(grid), dim3(attn::THREADS), AttnCfg<HD>::SMEM, st, m.q, m.qh,
+                         m.k, m.kh, m.v, out, T, heads, items);
+  return launch_kernel(attn_fwd_tcgen05<HD, false>, dim3(grid), dim3(attn::THREADS), AttnCfg<HD>::SMEM, st, m.q, m.qh,
+                       m.k, m.kh, m.v, out, T, heads, items);
+}
 
 int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, int T, cudaStream_t st) {
   if (prepare_attn_kernel() != SF_OK) return SF_ERR_CUDA;
@@ -483,11 +505,9 @@ int launch_attn(const AttnMaps& m, __nv_bfloat16* out, int64_t rows, int heads, 
   const int grid = (int)(items < attn_sm_count() ? items : attn_sm_count());
   cudaError_t err;
   if (m.hd == 64)
-    err = launch_kernel(attn_fwd_tcgen05<64>, dim3(grid), dim3(attn::THREADS), AttnCfg<64>::SMEM, st, m.q, m.qh,
-                           m.k, m.kh, m.v, out, T, heads, (int)items);
+    err = launch_attn_hd<64>(m, out, T, heads, (int)items, grid, st);
   else if (m.hd == 72)
-    err = launch_kernel(attn_fwd_tcgen05<72>, dim3(grid), dim3(attn::THREADS), AttnCfg<72>::SMEM, st, m.q, m.qh,
-                           m.k, m.kh, m.v, out, T, heads, (int)items);
+    err = launch_attn_hd<72>(m, out, T, heads, (int)items, grid, st);
   else
     return SF_ERR_PARAMETER;
   return err == cudaSuccess ? cuda_status() : SF_ERR_CUDA;

@@ -69,6 +69,7 @@ struct Params {
   float ln_eps;
   int T;
   int M;
+  int pdl;  // launched with programmatic serialisation (sf_internal.h g_pdl)
 };
 
 #if SF_TAIL2_TRACE
@@ -175,6 +176,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) pdl_trigger(p.pdl);  // the next kernel's CTAs may start their prologue
+  pdl_wait(p.pdl);                           // the attention output / residual stream are complete
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -585,7 +588,8 @@ int launch_block_tail(const void* attn, const void* wproj, const float* bproj, c
   rc |= make_tmap_bf16_2d(&trs, xres, D, (uint64_t)M, D, 64, 32, 128);
   rc |= make_tmap_bf16_2d(&tms, xmod_out, D, (uint64_t)M, D, 64, 32, 128);
   if (rc != SF_OK) return SF_ERR_CUDA;
-  Params p{xres, xmod_out, bproj, b1, b2, gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, T, (int)M};
+  Params p{xres, xmod_out, bproj, b1, b2, gate1, shift1, scale1, gate2, shift2, scale2, vec_stride, ln_eps, T, (int)M,
+           g_pdl ? 1 : 0};
   static int sms = 0;
   if (!sms) {
     int dev = 0;

@@ -105,6 +105,7 @@ struct RowSrc {
   const double* emb;        // stream: [S, E]; direct: [rows, E]
   const double* neg;        // stream + cfg: [S, E] or nullptr (zeros)
   int E;
+  int pdl;                  // launched with programmatic serialisation (sf_internal.h g_pdl)
 };
 
 // ============================================================ K1: conditioning
@@ -158,6 +159,8 @@ __global__ void __launch_bounds__(256) cond_h1_kernel(RowSrc src, int hidden, in
   extern __shared__ float sh[];
   float* f = sh;               // [freq_dim]
   float* red = sh + freq_dim;  // [8][32]
+  pdl_wait(src.pdl);
+  if (threadIdx.x == 0) pdl_trigger(src.pdl);
   const int64_t i = blockIdx.x;
   const double t = src.ts[i % src.R];
   const int half = freq_dim / 2;
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(256) cond_out_kernel(RowSrc src, int hidden, c
   float* h1 = sh;             // [hidden]
   float* e = sh + hidden;     // [64]
   float* red = e + 64;        // [8][32]
+  pdl_wait(src.pdl);
+  if (threadIdx.x == 0) pdl_trigger(src.pdl);
   const int64_t i = blockIdx.x;
   bool zero_emb;
   const double* er = cond_emb_row(src, i, &zero_emb);
@@ -260,7 +265,8 @@ template <int HID>
 __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_kernel(
     const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
     const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
-    float ln_eps, const __grid_constant__ CUtensorMap tmRes, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens) {
+    float ln_eps, const __grid_constant__ CUtensorMap tmRes, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens,
+    int pdl) {
   using PM = PatchMma<HID>;
   constexpr int NT = PM::NT, TROW = PM::TROW;
   extern __shared__ __align__(128) uint8_t psm[];
@@ -281,6 +287,10 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
     reinterpret_cast<float4*>(sPos)[idx] = make_float4(bv.x + pv.x, bv.y + pv.y, bv.z + pv.z, bv.w + pv.w);
   }
   __syncthreads();
+  // weights and the positional slice are no kernel's output: staged above under the previous
+  // kernel's tail; the latents and the adaLN vectors are read after the dependency wait
+  pdl_wait(pdl);
+  if (threadIdx.x == 0) pdl_trigger(pdl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   uint8_t* sY = psm + NT * 32 * 8 + PM::POS + warp * PM::WBUF;  // [16][TROW] staged bf16 residual rows
   float* sStat = reinterpret_cast<float*>(sY + 16 * TROW);      // [16][rstd, -mean * rstd]
@@ -426,8 +436,10 @@ __global__ void __launch_bounds__(256) ln_modulate_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ xmod,
                                                           const float* __restrict__ shift,
                                                           const float* __restrict__ scale, int64_t vec_stride,
-                                                          int64_t M, int T, float ln_eps) {
+                                                          int64_t M, int T, float ln_eps, int pdl) {
   constexpr int U = HID / 128;
+  pdl_wait(pdl);
+  if (threadIdx.x == 0) pdl_trigger(pdl);
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < M; tok += wstride) {
@@ -474,13 +486,16 @@ __global__ void __launch_bounds__(256) ln_modulate_kernel(const __nv_bfloat16* _
 int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const float* shift, const float* scale,
                        int64_t vec_stride, int64_t M, int N, int tokens_per_slot, float eps, cudaStream_t st) {
   const unsigned blocks = (unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16);
+  cudaError_t err;
   if (N == 384)
-    ln_modulate_kernel<384><<<blocks, 256, 0, st>>>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps);
+    err = launch_kernel(ln_modulate_kernel<384>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale, vec_stride, M,
+                        tokens_per_slot, eps, g_pdl ? 1 : 0);
   else if (N == 1152)
-    ln_modulate_kernel<1152><<<blocks, 256, 0, st>>>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps);
+    err = launch_kernel(ln_modulate_kernel<1152>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale, vec_stride,
+                        M, tokens_per_slot, eps, g_pdl ? 1 : 0);
   else
     return SF_ERR_PARAMETER;
-  return cuda_status();
+  return err == cudaSuccess ? cuda_status() : SF_ERR_CUDA;
 }
 
 // ============================================================ K10: final layer (+ CFG + Euler + emit + refill)
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     int P, int C, int64_t lat_rows, float* __restrict__ eps_out, const int64_t* __restrict__ ctl, int n, int64_t m,
     const double* __restrict__ stage_params, const int64_t* __restrict__ row_info, int cfg, float w,
     const double* __restrict__ w_streams, float* __restrict__ x_ring, const float* __restrict__ noise_in, uint64_t noise_seed, float* __restrict__ frames_out,
-    int64_t* __restrict__ frame_ids, int64_t total_tokens) {
+    int64_t* __restrict__ frame_ids, int64_t total_tokens, int pdl) {
   using FC = FinalCfg<HID>;
   constexpr int PK = FC::PK, TROW = FC::TROW, SROW = FC::SROW;
   extern __shared__ __align__(128) uint8_t fsm[];  // [PK][TROW] bf16 weights, bias[PK], barriers, tile rings
@@ -559,6 +574,8 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
   }
   if (threadIdx.x < PK) sbias[threadIdx.x] = fb[threadIdx.x];
   __syncthreads();
+  pdl_wait(pdl);  // (the weight TMA above reads no kernel's output)
+  if (threadIdx.x == 0) pdl_trigger(pdl);
   const int gw = HW / P, T = gw * gw;
   int64_t j = 0;
   if constexpr (STREAM) j = ctl[1];
@@ -794,6 +811,14 @@ enum ProfClass { P_PREPARE = 0, P_COND, P_ADALN, P_PATCH, P_QKV, P_ATTN, P_PROJ,
 
 // Called after every launch: counts launches and, in a profiled step, records
 // a CUDA event so each launch's duration can be attributed to its class.
+// Programmatic dependent launch for the step's kernels when the batch leaves SMs idle (<= 16
+// latent rows: the block tail then fills fewer than half of the 74 CTA pairs); see g_pdl.
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(int64_t rows) : prev(g_pdl) { g_pdl = rows <= 16; }
+  ~PdlScope() { g_pdl = prev; }
+};
+
 static void mark(sf_dit* h, int cls, cudaStream_t st) {
   h->launch_count++;
   if (!h->profiling) return;
@@ -897,13 +922,14 @@ static int run_blocks(sf_dit* h, int64_t rows, cudaStream_t st) {
 static int launch_cond(sf_dit* h, const RowSrc& src, int64_t rows, cudaStream_t st) {
   const sf_dit_config& c = h->cfg;
   const dim3 grid((unsigned)rows, (unsigned)((c.hidden + 31) / 32));
-  cond_h1_kernel<<<grid, 256, (c.freq_dim + 256) * sizeof(float), st>>>(src, c.hidden, c.freq_dim,
-                                                                        (const __nv_bfloat16*)h->w.t_w1t, h->w.t_b1,
-                                                                        h->h1);
+  if (launch_kernel(cond_h1_kernel, grid, dim3(256), (c.freq_dim + 256) * sizeof(float), st, src, c.hidden, c.freq_dim,
+                    (const __nv_bfloat16*)h->w.t_w1t, (const float*)h->w.t_b1, h->h1) != cudaSuccess)
+    return SF_ERR_CUDA;
   mark(h, P_COND, st);
-  cond_out_kernel<<<grid, 256, (c.hidden + 64 + 256) * sizeof(float), st>>>(
-      src, c.hidden, h->h1, (const __nv_bfloat16*)h->w.t_w2t, h->w.t_b2, (const __nv_bfloat16*)h->w.y_wt, h->w.y_b,
-      h->cond);
+  if (launch_kernel(cond_out_kernel, grid, dim3(256), (c.hidden + 64 + 256) * sizeof(float), st, src, c.hidden,
+                    (const float*)h->h1, (const __nv_bfloat16*)h->w.t_w2t, (const float*)h->w.t_b2,
+                    (const __nv_bfloat16*)h->w.y_wt, (const float*)h->w.y_b, h->cond) != cudaSuccess)
+    return SF_ERR_CUDA;
   mark(h, P_COND, st);
   return cuda_status();
 }
@@ -920,9 +946,10 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   int64_t per = std::max<int64_t>(1, slots / TG);
   per = std::min<int64_t>(per, (rows + wpb - 1) / wpb);
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
-  kern<<<(unsigned)(TG * per), 32 * wpb, sm, st>>>(x, lat_rows, c.latent_hw, c.patch, c.in_ch,
-                                                   (const __nv_bfloat16*)h->w.patch_w, h->w.patch_b, h->w.pos_embed,
-                                                   h->mod, h->mod_stride, c.ln_eps, h->pe_res, h->xmod, tokens);
+  if (launch_kernel(kern, dim3((unsigned)(TG * per)), dim3(32 * wpb), sm, st, x, lat_rows, c.latent_hw, c.patch, c.in_ch,
+                    (const __nv_bfloat16*)h->w.patch_w, (const float*)h->w.patch_b, (const float*)h->w.pos_embed,
+                    (const float*)h->mod, h->mod_stride, c.ln_eps, h->pe_res, h->xmod, tokens, g_pdl ? 1 : 0) != cudaSuccess)
+    return SF_ERR_CUDA;
   mark(h, P_PATCH, st);
   return cuda_status();
 }
@@ -941,10 +968,9 @@ static void launch_final(sf_dit* h, int64_t lat_rows, float* eps_out, const int6
   // persistent: one CTA per SM (the tile rings fill its shared memory), each warp walks groups
   const unsigned blocks = (unsigned)std::min<int64_t>((tokens / 16 + wpb - 1) / wpb, 148);
   auto fk = c.hidden == 384 ? final_layer_mma_kernel<384, STREAM> : final_layer_mma_kernel<1152, STREAM>;
-  fk<<<blocks, 32 * wpb, sm, st>>>(h->fin_x, h->fin_w, h->w.final_b, c.latent_hw, c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m,
-                              stage_params, row_info, cfg, w, w_streams, x_ring, noise_in, noise_seed, frames_out,
-                              frame_ids,
-                              tokens);
+  launch_kernel(fk, dim3(blocks), dim3(32 * wpb), sm, st, h->fin_x, h->fin_w, (const float*)h->w.final_b, c.latent_hw,
+                c.patch, c.in_ch, lat_rows, eps_out, ctl, n, m, stage_params, row_info, cfg, w, w_streams, x_ring,
+                noise_in, noise_seed, frames_out, frame_ids, tokens, g_pdl ? 1 : 0);
 }
 
 extern "C" {
@@ -1059,7 +1085,8 @@ int sf_dit_forward(sf_dit* h, int64_t rows, const float* x, const double* ts, co
   if (!h || rows < 1 || rows > h->max_rows) return SF_ERR_PARAMETER;
   cudaStream_t st = (cudaStream_t)stream;
   const sf_dit_config& c = h->cfg;
-  RowSrc src{nullptr, ts, rows, 0, row_embs, nullptr, c.embed_dim};
+  const PdlScope pdl(rows);
+  RowSrc src{nullptr, ts, rows, 0, row_embs, nullptr, c.embed_dim, g_pdl ? 1 : 0};
   int rc;
   if ((rc = launch_cond(h, src, rows, st))) return rc;
   if ((rc = run_forward_core(h, rows, st))) return rc;
@@ -1079,10 +1106,11 @@ static int stream_step_launches(sf_dit* h, int64_t* ctl, int64_t S, int32_t n, i
   const int64_t R = S * n;
   const int cfg = (w != 1.0) ? 1 : 0;
   const int64_t rows = cfg ? 2 * R : R;
+  const PdlScope pdl(rows);
   int rc;
   if ((rc = sf_stream_prepare(ctl, S, n, m, stage_params, row_info, row_t, st))) return rc;
   mark(h, P_PREPARE, st);
-  RowSrc src{row_info, row_t, R, cfg, emb, neg, c.embed_dim};
+  RowSrc src{row_info, row_t, R, cfg, emb, neg, c.embed_dim, g_pdl ? 1 : 0};
   if ((rc = launch_cond(h, src, rows, st))) return rc;
   if ((rc = run_forward_core(h, rows, st))) return rc;
   if ((rc = launch_patch(h, x_ring, R, rows, st))) return rc;

@@ -172,6 +172,7 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
   const int grid = tiles < sm_count() ? tiles : sm_count();
   EpiParams e = ep;
   e.M = M;
+  e.pdl = g_pdl ? 1 : 0;
   cudaError_t err;
   if constexpr (CTAS == 2) {
     const int num_n = N / BN, pair_tiles = num_n * ((M + 2 * C::BM - 1) / (2 * C::BM));
@@ -181,36 +182,14 @@ static int launch_one(const GemmMaps& maps, int M, int N, int K, const EpiParams
       pairs -= pairs % num_n;
       if (pairs < num_n) pairs = num_n;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    cfg.blockDim = dim3(C::THREADS);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W, CTAS>, maps, N, K, e);
+    err = launch_kernel_cl(gemm_bf16_tcgen05<BN, KIND, W, CTAS>, dim3((unsigned)(2 * pairs)), dim3(C::THREADS),
+                           C::SMEM_BYTES, st, 2u, maps, N, K, e);
     if (err == cudaSuccess) err = cudaGetLastError();
   } else if constexpr (KIND == EPI_RES_LN2) {
     // one cluster of XCH_CL CTAs per row tile in flight: grid = whole clusters
-    cudaLaunchConfig_t cfg = {};
     const int rows = (M + C::BM - 1) / C::BM, max_cl = sm_count() / XCH_CL;
-    cfg.gridDim = dim3((unsigned)(XCH_CL * (rows < max_cl ? rows : max_cl)));
-    cfg.blockDim = dim3(C::THREADS);
-    cfg.dynamicSmemBytes = C::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = XCH_CL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    err = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05<BN, KIND, W>, maps, N, K, e);
+    err = launch_kernel_cl(gemm_bf16_tcgen05<BN, KIND, W>, dim3((unsigned)(XCH_CL * (rows < max_cl ? rows : max_cl))),
+                           dim3(C::THREADS), C::SMEM_BYTES, st, (unsigned)XCH_CL, maps, N, K, e);
     if (err == cudaSuccess) err = cudaGetLastError();
   } else {
     err = launch_kernel(gemm_bf16_tcgen05<BN, KIND, W>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, maps, N,

@@ -64,6 +64,7 @@ struct EpiParams {
   // common
   int tokens_per_slot;  // rows of one latent (1024); tiles never straddle a slot
   int M;                // valid rows (tail rows of the last tile are masked)
+  int pdl;              // launched with programmatic serialisation (sf_internal.h g_pdl)
 };
 
 // TMA descriptors: A, B operands and up to three outputs
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) pdl_trigger(ep.pdl);  // the next kernel's CTAs may start their prologue
 
   if (warp == 0) {
     if (lane == 0) {
@@ -294,7 +296,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
       uint32_t it = 0;
       if constexpr (C::B_RES) {
         // the pair's column slice is fixed (the host sizes the grid to a multiple of N / BN
-        // pairs): this CTA's half of B, all K blocks, once; both halves complete on the leader
+        // pairs): this CTA's half of B, all K blocks, once; both halves complete on the leader.
+        // The weights are no kernel's output, so they load before the dependency wait, under the
+        // previous kernel's tail.
         if (t_first < t_limit) {
           if (leader) mbar_expect_tx(bfull, 2 * C::BRES_BYTES);
           for (int kb = 0; kb < C::KB_RES; ++kb)
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
                             tile_n0(t_first) + (int)crank * C::B_ROWS);
         }
       }
+      pdl_wait(ep.pdl);
       for (int tile = t_first; tile < t_limit; tile += t_stride) {
         const int m0 = tile_m0(tile), n0 = tile_n0(tile);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     // ---------------- MMA issuer: the whole warp runs the loop so descriptors
     // stay warp-uniform (uniform registers, no per-MMA R2UR waterfall); one
     // elected lane issues.  Descriptor address field = addr >> 4.
+    pdl_wait(ep.pdl);
     constexpr uint32_t idesc = idesc_bf16_f32(TWO_SM ? 256 : 128, C::MMA_N);
     const uint64_t a_desc0 = kmajor_desc<C::SWZ>(smem_u32(sA));
     const uint64_t b_desc0 = kmajor_desc<C::SWZ>(smem_u32(sB));
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
     }
   } else {
     // ---------------- epilogue warps
+    pdl_wait(ep.pdl);
     const uint32_t e = warp - 2;
     const uint32_t quarter = warp & 3;
     constexpr int EPI_THREADS = EPI_WARPS * 32;
