@@ -234,6 +234,7 @@ class StreamBatch:
                 raise ParameterError("the TAESD decoder takes 4x64x64 latents, one per stream (max_frames >= S)")
             self.images = torch.zeros(self.S, 3, 512, 512, dtype=torch.float32, device=dev)
         self._h2d_done = torch.cuda.Event()
+        self._io = None  # launch_host_io's side stream, events and double buffers (created on first use)
         self.stats = [RunStats() for _ in range(self.S)]
         self.j = 0
         self._stream = lambda: torch.cuda.current_stream().cuda_stream
@@ -386,12 +387,47 @@ class StreamBatch:
     def launch_host_io(self, noise_src: torch.Tensor, frames_dst: torch.Tensor) -> int:
         """End-to-end serving step with HOST buffers (noise="host"): async H2D of
         the admitted generation's noise from pinned ``noise_src`` [S, D], the
-        device step, async D2H of the emitted frames into pinned ``frames_dst``.
-        All three are ordered on the current stream; no host sync."""
-        self.noise_dev.copy_(noise_src, non_blocking=True)
+        device step, async D2H of the emitted frames into pinned ``frames_dst``;
+        no host sync.  The copies run on a side stream against double-buffered
+        device noise / frame buffers, so step j's D2H and step j+1's H2D overlap
+        the neighbouring steps' kernels (events order each buffer's reuse); call
+        ``io_join()`` to make the current stream wait for the outstanding copies.
+        ``sb.frames`` is the buffer the latest step wrote (rows of streams that retired no frame
+        this step, ``frame_ids == -1``, are stale, as with launch())."""
+        if self.noise != "host":
+            raise StateError("launch_host_io needs a StreamBatch built with noise='host'")
+        cur = torch.cuda.current_stream()
+        if self._io is None:
+            ev = lambda: [torch.cuda.Event(), torch.cuda.Event()]
+            self._io = {"cs": torch.cuda.Stream(device=self.device), "slot": 0,
+                        "noise": [self.noise_dev, torch.empty_like(self.noise_dev)],
+                        "frames": [self.frames, torch.zeros_like(self.frames)],
+                        "h2d": ev(), "step": ev(), "d2h": ev(), "used": [False, False]}
+        io = self._io
+        b, cs = io["slot"], io["cs"]
+        io["slot"] ^= 1
+        with torch.cuda.stream(cs):
+            if io["used"][b]:
+                cs.wait_event(io["step"][b])  # the step that read noise[b] two steps ago is done
+            io["noise"][b].copy_(noise_src, non_blocking=True)
+            io["h2d"][b].record(cs)
+        cur.wait_event(io["h2d"][b])
+        if io["used"][b]:
+            cur.wait_event(io["d2h"][b])  # frames[b]'s previous D2H has read it
+        self.noise_dev, self.frames = io["noise"][b], io["frames"][b]
         g = self.launch()
-        frames_dst.copy_(self.frames, non_blocking=True)
+        io["step"][b].record(cur)
+        with torch.cuda.stream(cs):
+            cs.wait_event(io["step"][b])
+            frames_dst.copy_(io["frames"][b], non_blocking=True)
+            io["d2h"][b].record(cs)
+        io["used"][b] = True
         return g
+
+    def io_join(self) -> None:
+        """Make the current stream wait for launch_host_io's outstanding copies."""
+        if self._io is not None:
+            torch.cuda.current_stream().wait_stream(self._io["cs"])
 
     def profile_step(self) -> dict:
         """One eager DiT step with a CUDA event after every launch: per kernel

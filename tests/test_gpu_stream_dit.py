@@ -199,3 +199,30 @@ def test_device_noise_refill_equals_philox_fill(setup, w):
         _lib.call("sf_philox_normal", ref.data_ptr(), S, model.dim, sb.noise_seed, j + 1, st)
         torch.cuda.synchronize()
         assert torch.equal(ring[:, (j + 1) % n], ref), j
+
+
+def test_launch_host_io_overlapped_copies_match_launch(setup):
+    """launch_host_io (H2D of the admission noise and D2H of the frames on a side stream, double-
+    buffered device noise / frames) gives the same frames as uploading the same noise and calling
+    launch() on the current stream, step for step (graph replay, 7 steps: both buffers reused)."""
+    sf, model = setup
+    S, n = 2, 4
+    sched = sf.build_time_window_schedule(num_windows=3, inference_steps=n)
+    cond = sf.make_conditioning(np.ones(8), guidance_scale=1.0)
+    mk = lambda: sf.StreamBatch(model, sched, n, num_streams=S, cond=cond, seed=21, dtype=np.float32, noise="host")
+    a, b = mk(), mk()
+    g = torch.Generator().manual_seed(4)
+    noises = [torch.randn(S, model.dim, generator=g).pin_memory() for _ in range(7)]
+    dsts = [torch.empty(S, model.dim).pin_memory() for _ in range(7)]
+    for j in range(7):
+        a.noise_dev.copy_(noises[j].cuda())
+        a.launch()
+        want = a.frames.cpu()
+        b.launch_host_io(noises[j], dsts[j])
+        b.io_join()
+        torch.cuda.synchronize()
+        assert torch.equal(a.frame_ids, b.frame_ids), j
+        ok = (a.frame_ids >= 0).cpu()  # streams that retired a frame this step
+        assert torch.equal(dsts[j][ok], want[ok]), j
+        assert torch.equal(b.frames.cpu()[ok], want[ok]), j
+    assert ok.all()  # steady state reached
