@@ -503,12 +503,12 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 // accumulate): one warp per 16 consecutive tokens (T % 16 == 0), N = 16 output
 // features as two n8 tiles, K = HID in 16-wide steps.  The projection is ~0.4% of the
 // network's FLOPs, so the legacy HMMA rate is ample; what matters is that xmod (the
-// kernel's only large input, T*HID bf16 per row) streams at HBM rate.  Each warp owns a
-// two-deep ring of 16-token tiles in shared memory filled by TMA (one box per tile) and
-// completing on a per-buffer mbarrier: the loads of the next two groups are in flight while
-// the warp runs the projection and the Euler/emit/refill epilogue of the current one, and
-// the epilogue's own loads (ring row, noise, stage parameters) are issued before the tile
-// wait.  The tensor map views a token row as NSEG = HID/192 segments of 192 elements and
+// kernel's only large input, T*HID bf16 per row) streams at HBM rate.  Each warp (up to 12 per
+// CTA, one CTA per SM) owns a 16-token tile buffer in shared memory filled by TMA (one box per
+// tile) and completing on an mbarrier: the buffer is refilled with the warp's next group as soon
+// as the projection has read it, so that load is in flight during the Euler/emit/refill
+// epilogue, and the epilogue's own loads (ring row, noise, stage parameters) are issued before
+// the tile wait.  The tensor map views a token row as NSEG = HID/192 segments of 192 elements and
 // the box is 208 elements wide: TMA zero-fills the 16 out-of-bounds elements, so every
 // staged segment is 416 B and consecutive token rows start 64 B apart modulo 128 B -- the
 // fragment loads of a quarter-warp (two token rows) are conflict-free without a per-row
@@ -519,20 +519,25 @@ int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const flo
 // {8+2c, 9+2c}.
 template <int HID>
 struct FinalCfg {
+  // one tile buffer per warp (refilled right after its fragments are loaded, so the next group's
+  // load overlaps this group's epilogue) and up to 12 warps: more warps in flight beat a deeper
+  // per-warp ring (ncu: 26.5 vs 29.3 us with two buffers x 8 warps, profiles/r02s3/experiments.md)
+  static constexpr int ST = 1;
+  static constexpr int MAXW = 12;
   static constexpr int PK = 16;
   static constexpr int SEG = 192, SEG_BOX = 208;       // elements per segment / per staged segment
   static constexpr int NSEG = HID / SEG;
   static constexpr int SROW = SEG_BOX * 2;             // staged segment (bytes)
   static constexpr int TROW = NSEG * SROW;             // staged token / weight row (bytes)
   static constexpr int TILE = 16 * TROW;
-  static constexpr int HEAD = ((PK * TROW + PK * 4 + (2 * 8 + 1) * 8) + 127) / 128 * 128;  // weights, bias, barriers
+  static constexpr int HEAD = ((PK * TROW + PK * 4 + (ST * MAXW + 1) * 8) + 127) / 128 * 128;  // weights, bias, barriers
   static_assert(HID % SEG == 0 && (TROW % 128) == 64, "token rows must alternate 64-byte bank halves");
-  // warps per CTA: two ring buffers per warp of 1 (2 with CFG: cond + uncond rows) tiles
+  // warps per CTA: ST ring buffers per warp of 1 (2 with CFG: cond + uncond rows) tiles
   static int warps(int tiles) {
-    const int w = (227 * 1024 - HEAD) / (2 * tiles * TILE);
-    return w > 8 ? 8 : (w < 1 ? 1 : w);
+    const int w = (227 * 1024 - HEAD) / (ST * tiles * TILE);
+    return w > MAXW ? MAXW : (w < 1 ? 1 : w);
   }
-  static size_t smem(int tiles) { return HEAD + (size_t)warps(tiles) * 2 * tiles * TILE; }
+  static size_t smem(int tiles) { return HEAD + (size_t)warps(tiles) * ST * tiles * TILE; }
 };
 
 // [rows, HID] bf16 -> [rows * NSEG, 192] with 208-wide boxes of 16 * NSEG segment rows
@@ -543,7 +548,7 @@ int make_final_map(CUtensorMap* m, const void* p, int64_t rows) {
 }
 
 template <int HID, bool STREAM>
-__global__ void __launch_bounds__(256) final_layer_mma_kernel(
+__global__ void __launch_bounds__(32 * FinalCfg<HID>::MAXW) final_layer_mma_kernel(
     const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, const float* __restrict__ fb, int HW,
     int P, int C, int64_t lat_rows, float* __restrict__ eps_out, const int64_t* __restrict__ ctl, int n, int64_t m,
     const double* __restrict__ stage_params, const int64_t* __restrict__ row_info, int cfg, float w,
@@ -557,9 +562,9 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const int WARPS = blockDim.x >> 5;
   const int NT = (STREAM && cfg) ? 2 : 1;  // tiles per group: cond (+ uncond) rows
-  uint8_t* ring = fsm + FC::HEAD + (size_t)warp * 2 * NT * FC::TILE;
-  uint64_t* bar = bars + 2 * warp;
-  uint64_t* wbar = bars + 2 * WARPS;
+  uint8_t* ring = fsm + FC::HEAD + (size_t)warp * FC::ST * NT * FC::TILE;
+  uint64_t* bar = bars + FC::ST * warp;
+  uint64_t* wbar = bars + FC::ST * WARPS;
   if (threadIdx.x == 0) {
     tma_prefetch(&tmX);
     mbar_init(wbar, 1);
@@ -568,8 +573,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     tma_load_2d(fsm, &tmW, wbar, 0, 0);
   }
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < FC::ST; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   if (threadIdx.x < PK) sbias[threadIdx.x] = fb[threadIdx.x];
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
     const uint8_t* a0 = tile + g * TROW + 16 * c;
     const uint8_t* a1 = a0 + 8 * TROW;
     constexpr int NCH = HID / 32;  // 32 K elements (two k-steps) per 16-byte lane run; 6 per segment
-#pragma unroll 6
+#pragma unroll 2
     for (int ch = 0; ch < NCH; ++ch) {
       const int off = (ch / 6) * SROW + (ch % 6) * 64;
       const uint4 xa = *reinterpret_cast<const uint4*>(a0 + off);
@@ -630,11 +634,11 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
 
   const int64_t D = (int64_t)C * HW * HW;
   const int64_t gw0 = (int64_t)blockIdx.x * WARPS + warp;
-  if (gw0 < groups) issue(gw0, 0);
-  if (gw0 + gstride < groups) issue(gw0 + gstride, 1);
+  for (int k = 0; k < FC::ST; ++k)
+    if (gw0 + k * gstride < groups) issue(gw0 + k * gstride, k);
   int it = 0;
   for (int64_t grp = gw0; grp < groups; grp += gstride, ++it) {
-    const int b = it & 1;
+    const int b = it % FC::ST;
     const int64_t tok0 = grp * 16, lr = tok0 / T;
     const int tau0 = (int)(tok0 % T);
     // this lane's 8 latent elements u = 4 nt + i: token tau0 + g + 8 (i >> 1), feature
@@ -686,7 +690,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
       if (admit && !noise_in) philox_normal_group8(noise_seed + (uint64_t)s, j + 1, idx, lane, nz);
     }
     if (it == 0) mbar_wait(wbar, 0);  // weights staged
-    mbar_wait(&bar[b], (it >> 1) & 1);
+    mbar_wait(&bar[b], (it / FC::ST) & 1);
     float e[2][4];
     project(ring + b * NT * FC::TILE, e);
     if constexpr (STREAM) {
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(256) final_layer_mma_kernel(
       }
     }
     __syncwarp();  // every lane's fragment loads of buffer b are done: refill it
-    if (grp + 2 * gstride < groups) issue(grp + 2 * gstride, b);
+    if (grp + FC::ST * gstride < groups) issue(grp + FC::ST * gstride, b);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
