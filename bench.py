@@ -294,8 +294,6 @@ class Clocks:
         self.t0 = time.time()
 
     def stop(self) -> dict:
-        import datetime
-
         self.t1 = time.time()
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -306,9 +304,21 @@ class Clocks:
         except Exception:
             self.proc.kill()
         self.fh.close()
+        with open(self.path) as fh:
+            out = self.parse(fh.read().splitlines(), self.t0, self.t1)
+        os.unlink(self.path)
+        return out
+
+    @staticmethod
+    def parse(lines, t0, t1) -> dict:
+        """Clock summary of `nvidia-smi --query-gpu=<FIELDS> --format=csv,noheader,nounits` lines:
+        the samples stamped inside [t0, t1] (or the first one after t0), median SM clock, the
+        throttle reasons seen."""
+        import datetime
+
         rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for line in lines:
             p = [x.strip() for x in line.split(",")]
             if len(p) < 10:
                 continue
@@ -318,12 +328,10 @@ class Clocks:
                                                              if v.lower().startswith("active")}))
             except ValueError:
                 continue
-        os.unlink(self.path)
-        t0 = self.t0 if self.t0 is not None else -1e18
-        inside = [r for r in rows if t0 <= r[0] <= self.t1]
+        t0 = t0 if t0 is not None else -1e18
+        inside = [r for r in rows if t0 <= r[0] <= t1]
         if not inside:  # region shorter than the sampling interval: the first sample after its start
-            after = [r for r in rows if r[0] >= t0]
-            inside = after[:1]
+            inside = [r for r in rows if r[0] >= t0][:1]
         sm = [r[1] for r in inside]
         reasons = set().union(*[r[3] for r in inside]) if inside else set()
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": inside[-1][2] if inside else None,

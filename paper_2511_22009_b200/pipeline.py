@@ -395,7 +395,7 @@ class StreamBatch:
         ``sb.frames`` is the buffer the latest step wrote (rows of streams that retired no frame
         this step, ``frame_ids == -1``, are stale, as with launch())."""
         if self.noise != "host":
-            raise StateError("launch_host_io needs a StreamBatch built with noise='host'")
+            raise ParameterError("launch_host_io needs a StreamBatch built with noise='host'")
         cur = torch.cuda.current_stream()
         if self._io is None:
             ev = lambda: [torch.cuda.Event(), torch.cuda.Event()]
