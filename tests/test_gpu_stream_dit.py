@@ -226,3 +226,25 @@ def test_launch_host_io_overlapped_copies_match_launch(setup):
         assert torch.equal(dsts[j][ok], want[ok]), j
         assert torch.equal(b.frames.cpu()[ok], want[ok]), j
     assert ok.all()  # steady state reached
+
+
+def test_batch_of_streams_equals_single_stream_batches():
+    """One DiT StreamBatch of 5 streams (20 network rows: plain launches) gives every stream the
+    frames of its own single-stream batch (4 rows: the small-batch programmatic-dependent-launch
+    path), bit for bit: row independence across batch sizes and launch modes."""
+    import paper_2511_22009_b200 as sf
+    from paper_2511_22009_b200.dit import DIT_S2
+
+    model = sf.DiTVelocityModel(DIT_S2, seed=9, max_rows=20, bias_std=0.02)
+    S, n, m = 5, 4, 6
+    sched = sf.build_time_window_schedule(num_windows=4, inference_steps=n)
+    rng = np.random.default_rng(3)
+    conds = [sf.make_conditioning(rng.standard_normal(8)) for _ in range(S)]
+    seeds = [100 + 7 * s for s in range(S)]
+    big = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, m=m, dtype=np.float32)()
+    for s in range(S):
+        one = sf.StreamBatch(model, sched, n, num_streams=1, cond=[conds[s]], seed=[seeds[s]], m=m,
+                             dtype=np.float32)()[0]
+        assert [r.id for r in one] == [r.id for r in big[s]]
+        for a, b in zip(one, big[s]):
+            assert np.array_equal(a.latent, b.latent), (s, a.id)
