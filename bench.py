@@ -187,7 +187,7 @@ def run_mock(args):
                  sf._lib.SF_F64 if dt == np.float64 else sf._lib.SF_F32, sb.x_ring.data_ptr(),
                  sb.stage_params.data_ptr(), sb.row_info.data_ptr(), sb.row_t.data_ptr(), model.seed,
                  sb.emb.data_ptr(), None, 8, sb.w, None, sb.noise_dev.data_ptr(), sb.frames.data_ptr(),
-                 sb.frame_ids.data_ptr(), st)
+                 sb.frame_ids.data_ptr(), sb.mock_keys.data_ptr(), st)
     ev[3].record()
     torch.cuda.synchronize()
     sb.j += 1

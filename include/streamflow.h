@@ -141,11 +141,13 @@ int sf_stream_prepare(int64_t* ctl, int64_t S, int32_t n, int64_t m, const doubl
  *   j+1 >= m.  emb / neg: [S, E] fp64 (neg may be NULL = zeros,
  *   models.py:258-260).  model_seed: SeededMockModel seed.  w_streams: NULL (every
  *   stream uses w) or device fp64 [S] per-stream guidance scales (a stream with
- *   w_s == 1 runs unguided, exactly as its own run_stream would). */
+ *   w_s == 1 runs unguided, exactly as its own run_stream would).  keys: device scratch of
+ *   2 * S * n uint64 (the step's blake2b row keys, computed by a first launch). */
 int sf_stream_mock_step(const int64_t* ctl, int64_t S, int32_t n, int64_t m, int64_t D, int x_dtype, void* x_ring,
                         const double* stage_params, const int64_t* row_info, const double* row_t, int64_t model_seed,
                         const double* emb, const double* neg, int32_t E, double w, const double* w_streams,
-                        const double* noise_in, void* frames_out, int64_t* frame_ids, void* stream);
+                        const double* noise_in, void* frames_out, int64_t* frame_ids, uint64_t* keys,
+                        void* stream);
 
 /* Write generation-0 noise into slot 0 of every stream and reset ctl (j = 0). */
 int sf_stream_reset(int64_t* ctl, int64_t S, int32_t n, int64_t D, int x_dtype, void* x_ring,

@@ -47,7 +47,7 @@ SIGNATURES = {
     "sf_mock_eps": [_vp, _i64, _i64, _vp, _vp],
     "sf_stream_prepare": [_vp, _i64, _i32, _i64, _vp, _vp, _vp, _vp],
     "sf_stream_mock_step": [_vp, _i64, _i32, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _i64,
-                            _vp, _vp, _i32, _f64, _vp, _vp, _vp, _vp, _vp],
+                            _vp, _vp, _i32, _f64, _vp, _vp, _vp, _vp, _vp, _vp],
     "sf_stream_reset": [_vp, _i64, _i32, _i64, C.c_int, _vp, _vp, _vp],
     "sf_gemm_bf16": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp],
     "sf_gemm_qkv": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, C.c_float, _vp],

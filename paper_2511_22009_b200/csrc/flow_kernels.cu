@@ -281,14 +281,43 @@ __global__ void stream_prepare_kernel(int64_t* ctl, int64_t S, int n, int64_t m,
   }
 }
 
+// The mock's blake2b row keys of every ring row, one thread per (row, cond / uncond key): computed
+// once per step in parallel instead of by one thread of each of the step kernel's blocks (the
+// serial blake2b on that thread bounded the step: 360 -> see profiles/r02s3/experiments.md).
+// keys[2 r + 1] = cond key, keys[2 r] = uncond key (guided rows only).
+__global__ void stream_mock_keys_kernel(int64_t R, const int64_t* __restrict__ row_info,
+                                        const double* __restrict__ row_t, int64_t seed, const double* emb,
+                                        const double* neg, int E, double w, const double* __restrict__ w_streams,
+                                        uint64_t* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 2 * R) return;
+  const int64_t r = i >> 1;
+  const bool cond = i & 1;
+  if (row_info[r * 4 + 2] == 0) return;  // inactive row: no eps
+  const int64_t g = row_info[r * 4 + 1], s = row_info[r * 4 + 3];
+  const double ws = w_streams ? w_streams[s] : w;
+  if (!cond && ws == 1.0) return;  // unguided (pipeline.py:113): no uncond half
+  // apply_cfg (models.py:257-268): the uncond half uses the negative embedding (zeros when absent)
+  double zeros[64];
+  const double* e = emb + s * E;
+  if (!cond) {
+    if (neg) {
+      e = neg + s * E;
+    } else {
+      for (int k = 0; k < E; ++k) zeros[k] = 0.0;
+      e = zeros;
+    }
+  }
+  keys[i] = mock_row_key(seed, g, row_t[r], e, E);
+}
+
 // One block = (chunk of D, ring row).  Guided mock eps -> Euler -> emit -> refill.
 template <typename TX>
 __global__ void stream_mock_step_kernel(const int64_t* ctl, int64_t S, int n, int64_t m, int64_t D, TX* x_ring,
                                         const double* __restrict__ stage_params, const int64_t* __restrict__ row_info,
-                                        const double* __restrict__ row_t, int64_t seed, const double* emb,
-                                        const double* neg, int E, double w, const double* __restrict__ w_streams,
-                                        const double* __restrict__ noise_in, TX* frames_out, int64_t* frame_ids) {
-  __shared__ uint64_t s_keys[2];
+                                        const uint64_t* __restrict__ keys, double w,
+                                        const double* __restrict__ w_streams, const double* __restrict__ noise_in,
+                                        TX* frames_out, int64_t* frame_ids) {
   const int64_t r = blockIdx.y;
   const int64_t j = ctl[1];
   const int64_t stage = row_info[r * 4 + 0];
@@ -301,27 +330,15 @@ __global__ void stream_mock_step_kernel(const int64_t* ctl, int64_t S, int n, in
   const bool retiring = active && (stage + 1 == n);
   const double ws = w_streams ? w_streams[s] : w;  // this stream's guidance scale
   const bool guided = (ws != 1.0);                 // pipeline.py:113
-  if (active && threadIdx.x == 0) {
-    const double t = row_t[r];
-    // apply_cfg (models.py:257-268): uncond half uses the negative embedding (zeros when absent)
-    s_keys[1] = mock_row_key(seed, g, t, emb + s * E, E);
-    if (guided) {
-      double zeros[64];
-      const double* ne = neg ? neg + s * E : zeros;
-      if (!neg)
-        for (int i = 0; i < E; ++i) zeros[i] = 0.0;
-      s_keys[0] = mock_row_key(seed, g, t, ne, E);
-    }
-  }
+  const uint64_t key_c = active ? keys[2 * r + 1] : 0, key_u = (active && guided) ? keys[2 * r] : 0;
   if (blockIdx.x == 0 && threadIdx.x == 0 && refill_slot) frame_ids[s] = retiring ? g : -1;
-  __syncthreads();
   const StepCoef64 c = load_coef(stage_params + stage * SF_PARAM_STRIDE);
   TX* xr = x_ring + r * D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
     if (active) {
-      double e = splitmix_unit(s_keys[1], (uint64_t)i);
+      double e = splitmix_unit(key_c, (uint64_t)i);
       if (guided) {  // handle_cfg (models.py:288-293), fp64 like the mock's output
-        const double eu = splitmix_unit(s_keys[0], (uint64_t)i);
+        const double eu = splitmix_unit(key_u, (uint64_t)i);
         e = __dadd_rn(eu, __dmul_rn(ws, __dsub_rn(e, eu)));
       }
       const TX xn = euler(xr[i], cast_to<TX>(e), c);
@@ -470,20 +487,23 @@ int sf_stream_prepare(int64_t* ctl, int64_t S, int32_t n, int64_t m, const doubl
 int sf_stream_mock_step(const int64_t* ctl, int64_t S, int32_t n, int64_t m, int64_t D, int x_dtype, void* x_ring,
                         const double* stage_params, const int64_t* row_info, const double* row_t, int64_t model_seed,
                         const double* emb, const double* neg, int32_t E, double w, const double* w_streams,
-                        const double* noise_in, void* frames_out, int64_t* frame_ids, void* stream) {
-  if (S < 1 || n < 1 || m < 1 || D < 1 || E < 1 || E > 64 || S * n > 65535) return SF_ERR_PARAMETER;
-  dim3 grid(grid_for(D, 256) > 16 ? 16 : grid_for(D, 256), (unsigned)(S * n));
+                        const double* noise_in, void* frames_out, int64_t* frame_ids, uint64_t* keys,
+                        void* stream) {
+  if (S < 1 || n < 1 || m < 1 || D < 1 || E < 1 || E > 64 || S * n > 65535 || !keys) return SF_ERR_PARAMETER;
+  if (x_dtype != SF_F64 && x_dtype != SF_F32) return SF_ERR_PARAMETER;
+  const int64_t R = S * n;
   cudaStream_t st = (cudaStream_t)stream;
+  stream_mock_keys_kernel<<<(unsigned)((2 * R + 127) / 128), 128, 0, st>>>(R, row_info, row_t, model_seed, emb, neg, E,
+                                                                          w, w_streams, keys);
+  dim3 grid(grid_for(D, 256) > 16 ? 16 : grid_for(D, 256), (unsigned)R);
   if (x_dtype == SF_F64)
     stream_mock_step_kernel<double><<<grid, 256, 0, st>>>(ctl, S, n, m, D, (double*)x_ring, stage_params, row_info,
-                                                          row_t, model_seed, emb, neg, E, w, w_streams,
-                                                          noise_in, (double*)frames_out, frame_ids);
-  else if (x_dtype == SF_F32)
-    stream_mock_step_kernel<float><<<grid, 256, 0, st>>>(ctl, S, n, m, D, (float*)x_ring, stage_params, row_info,
-                                                         row_t, model_seed, emb, neg, E, w, w_streams,
-                                                         noise_in, (float*)frames_out, frame_ids);
+                                                          keys, w, w_streams, noise_in, (double*)frames_out,
+                                                          frame_ids);
   else
-    return SF_ERR_PARAMETER;
+    stream_mock_step_kernel<float><<<grid, 256, 0, st>>>(ctl, S, n, m, D, (float*)x_ring, stage_params, row_info,
+                                                         keys, w, w_streams, noise_in, (float*)frames_out,
+                                                         frame_ids);
   return cuda_status();
 }
 

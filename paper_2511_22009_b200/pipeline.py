@@ -235,6 +235,8 @@ class StreamBatch:
             self.images = torch.zeros(self.S, 3, 512, 512, dtype=torch.float32, device=dev)
         self._h2d_done = torch.cuda.Event()
         self._io = None  # launch_host_io's side stream, events and double buffers (created on first use)
+        # the mock step's per-row blake2b keys (cond / uncond), device scratch
+        self.mock_keys = torch.empty(2 * R, dtype=torch.int64, device=dev) if self.kind == "mock" else None
         self.stats = [RunStats() for _ in range(self.S)]
         self.j = 0
         self._stream = lambda: torch.cuda.current_stream().cuda_stream
@@ -322,7 +324,7 @@ class StreamBatch:
                           self.stage_params.data_ptr(), self.row_info.data_ptr(), self.row_t.data_ptr(),
                           self.model.seed, self.emb.data_ptr(), None if self.neg is None else self.neg.data_ptr(),
                           self.model.embed_dim, self.w, self._wptr(), self.noise_dev.data_ptr(),
-                          self.frames.data_ptr(), self.frame_ids.data_ptr(), st)
+                          self.frames.data_ptr(), self.frame_ids.data_ptr(), self.mock_keys.data_ptr(), st)
             else:
                 self._generic_step(j)
         lo, hi = max(0, j - n + 1), min(j, m - 1)
