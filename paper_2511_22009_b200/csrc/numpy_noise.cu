@@ -10,9 +10,11 @@
 // t of every 256-draw round (its own LCG state, advanced by the 256-step jump
 // (A^256, c_256) each round).  ~99% of draws take the ziggurat fast path and map
 // to one output each; the rare rejection draws (wedge / tail, which consume
-// further uniforms from the same stream) are resolved in sequence order by one
-// thread, stepping the LCG from the special draw's saved state.  A block scan
-// over "this draw produces an output" gives every output its index.
+// further uniforms from the same stream) are evaluated speculatively by their own
+// threads (stepping the LCG from their own state), and one thread walks them in
+// sequence order to decide which are live (a draw consumed by an earlier rejection
+// draw is not).  A block scan over "this draw produces an output" gives every
+// output its index.
 //
 // Floating point: every operation that decides or forms an output is written with
 // explicit _rn intrinsics in numpy's literal order (no FMA contraction), except the
@@ -207,9 +209,9 @@ __global__ void __launch_bounds__(T) numpy_normal_kernel(const int64_t* __restri
                                                          OUT* __restrict__ out_all) {
   __shared__ uint64_t s_ki[256];
   __shared__ double s_wi[256], s_fi[256];
-  __shared__ u128 s_state[T];
   __shared__ double s_val[T];
-  __shared__ uint32_t s_special[T / 32], s_consumed[T / 32], s_accept[T / 32];
+  __shared__ uint32_t s_special[T / 32], s_spec_acc[T / 32], s_consumed[T / 32], s_accept[T / 32];
+  __shared__ long long s_pos[T];  // a rejection draw's first draw after the ones it consumes
   __shared__ int s_cnt[T / 32];
   __shared__ u128 s_seed[2];
   __shared__ long long s_skip;
@@ -241,13 +243,50 @@ __global__ void __launch_bounds__(T) numpy_normal_kernel(const int64_t* __restri
   while (out_base < D) {
     const Draw d = ziggurat_draw(xsl_rr(st), s_wi);
     const bool fast = d.rabs < s_ki[d.idx];
-    s_state[t] = st;
+    // A rejection draw (wedge / tail, distributions.c random_standard_normal) is evaluated by its
+    // own thread, speculatively (as if no earlier rejection draw consumed it): its outcome and the
+    // extra draws it consumes depend only on the raw stream, so one thread then only has to walk
+    // the round's rejection draws in sequence order to decide which are live.
+    bool acc = false;
+    if (!fast) {
+      u128 cs = st;
+      long long pos = round_base + t + 1;
+      double val = d.x;
+      if (d.idx == 0) {
+        for (;;) {
+          cs = step(cs, inc);
+          const double u1 = next_double(xsl_rr(cs));
+          cs = step(cs, inc);
+          const double u2 = next_double(xsl_rr(cs));
+          pos += 2;
+          const double xx = __dmul_rn(-ZIG_INV_R, glibc_log1p(-u1));
+          const double yy = -glibc_log1p(-u2);
+          if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+            val = ((d.rabs >> 8) & 1) ? -__dadd_rn(ZIG_R, xx) : __dadd_rn(ZIG_R, xx);
+            break;
+          }
+        }
+        acc = true;
+      } else {
+        cs = step(cs, inc);
+        const double u = next_double(xsl_rr(cs));
+        pos += 1;
+        const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(s_fi[d.idx - 1], s_fi[d.idx]), u), s_fi[d.idx]);
+        acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, d.x), d.x));
+      }
+      s_pos[t] = pos;
+      s_val[t] = val;
+    }
     const uint32_t spec = __ballot_sync(0xffffffffu, !fast);
-    if (lane == 0) s_special[w] = spec;
+    const uint32_t spec_acc = __ballot_sync(0xffffffffu, !fast && acc);
+    if (lane == 0) {
+      s_special[w] = spec;
+      s_spec_acc[w] = spec_acc;
+    }
     __syncthreads();
     if (t == 0) {
-      // resolve the rejection draws of this round in sequence order (distributions.c
-      // random_standard_normal); draws a special consumes are not outputs of their own.
+      // the live rejection draws of this round, in sequence order; draws a live one consumes are
+      // not outputs of their own
       long long skip = s_skip;
       const long long round_end = round_base + T;
       for (int k = 0; k < T / 32; ++k) s_consumed[k] = s_accept[k] = 0;
@@ -264,39 +303,10 @@ __global__ void __launch_bounds__(T) numpy_normal_kernel(const int64_t* __restri
           m &= m - 1;
           const long long g = round_base + p;
           if (g < skip) continue;
-          u128 cs = s_state[p];
-          const Draw e = ziggurat_draw(xsl_rr(cs), s_wi);
-          long long pos = g + 1;
-          bool acc;
-          double val = e.x;
-          if (e.idx == 0) {
-            for (;;) {
-              cs = step(cs, inc);
-              const double u1 = next_double(xsl_rr(cs));
-              cs = step(cs, inc);
-              const double u2 = next_double(xsl_rr(cs));
-              pos += 2;
-              const double xx = __dmul_rn(-ZIG_INV_R, glibc_log1p(-u1));
-              const double yy = -glibc_log1p(-u2);
-              if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-                val = ((e.rabs >> 8) & 1) ? -__dadd_rn(ZIG_R, xx) : __dadd_rn(ZIG_R, xx);
-                break;
-              }
-            }
-            acc = true;
-          } else {
-            cs = step(cs, inc);
-            const double u = next_double(xsl_rr(cs));
-            pos += 1;
-            const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(s_fi[e.idx - 1], s_fi[e.idx]), u), s_fi[e.idx]);
-            acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, e.x), e.x));
-          }
+          const long long pos = s_pos[p];
           mark(g + 1, pos);
           skip = pos;
-          if (acc) {
-            s_accept[k] |= 1u << (p & 31);
-            s_val[p] = val;
-          }
+          s_accept[k] |= s_spec_acc[k] & (1u << (p & 31));
         }
       }
       s_skip = skip > round_end ? skip : round_end;
