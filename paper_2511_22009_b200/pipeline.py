@@ -234,7 +234,7 @@ class StreamBatch:
                 raise ParameterError("the TAESD decoder takes 4x64x64 latents, one per stream (max_frames >= S)")
             self.images = torch.zeros(self.S, 3, 512, 512, dtype=torch.float32, device=dev)
         self._h2d_done = torch.cuda.Event()
-        self._io = None  # launch_host_io's side stream, events and double buffers (created on first use)
+        self._io = None  # launch_host_io's copy streams, events and double buffers (created on first use)
         # the mock step's per-row blake2b keys (cond / uncond), device scratch
         self.mock_keys = torch.empty(2 * R, dtype=torch.int64, device=dev) if self.kind == "mock" else None
         self.stats = [RunStats() for _ in range(self.S)]
@@ -390,7 +390,7 @@ class StreamBatch:
         """End-to-end serving step with HOST buffers (noise="host"): async H2D of
         the admitted generation's noise from pinned ``noise_src`` [S, D], the
         device step, async D2H of the emitted frames into pinned ``frames_dst``;
-        no host sync.  The copies run on a side stream against double-buffered
+        no host sync.  The copies run on two side streams (H2D, D2H) against double-buffered
         device noise / frame buffers, so step j's D2H and step j+1's H2D overlap
         the neighbouring steps' kernels (events order each buffer's reuse); call
         ``io_join()`` to make the current stream wait for the outstanding copies.
@@ -401,7 +401,8 @@ class StreamBatch:
         cur = torch.cuda.current_stream()
         if self._io is None:
             ev = lambda: [torch.cuda.Event(), torch.cuda.Event()]
-            self._io = {"cs": torch.cuda.Stream(device=self.device), "slot": 0,
+            self._io = {"cs": torch.cuda.Stream(device=self.device), "cs_out": torch.cuda.Stream(device=self.device),
+                        "slot": 0,
                         "noise": [self.noise_dev, torch.empty_like(self.noise_dev)],
                         "frames": [self.frames, torch.zeros_like(self.frames)],
                         "h2d": ev(), "step": ev(), "d2h": ev(), "used": [False, False]}
@@ -419,10 +420,11 @@ class StreamBatch:
         self.noise_dev, self.frames = io["noise"][b], io["frames"][b]
         g = self.launch()
         io["step"][b].record(cur)
-        with torch.cuda.stream(cs):
-            cs.wait_event(io["step"][b])
+        co = io["cs_out"]  # D2H on its own stream: it overlaps the next step's H2D (full-duplex link)
+        with torch.cuda.stream(co):
+            co.wait_event(io["step"][b])
             frames_dst.copy_(io["frames"][b], non_blocking=True)
-            io["d2h"][b].record(cs)
+            io["d2h"][b].record(co)
         io["used"][b] = True
         return g
 
@@ -430,6 +432,7 @@ class StreamBatch:
         """Make the current stream wait for launch_host_io's outstanding copies."""
         if self._io is not None:
             torch.cuda.current_stream().wait_stream(self._io["cs"])
+            torch.cuda.current_stream().wait_stream(self._io["cs_out"])
 
     def profile_step(self) -> dict:
         """One eager DiT step with a CUDA event after every launch: per kernel
