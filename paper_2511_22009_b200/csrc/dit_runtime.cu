@@ -251,7 +251,9 @@ struct PatchMma {
   static constexpr int TROW = NSEG * 416;                     // staged row (bytes)
   static constexpr int WARPS = HID <= 384 ? 5 : 2;            // per CTA (2 CTAs per SM at hidden 384)
   static constexpr int WBUF = 16 * TROW + 16 * 2 * 4;         // per warp: 16 rows + (mean, rstd) x 16
-  static constexpr int POS = 16 * HID * 4;                    // the CTA's pos (+ bias) slice, fp32
+  static constexpr int PROW = HID + 4;                        // pos row (floats), padded: the LDS.128 of rows
+                                                              // g and g+1 land on disjoint banks (was 2-way)
+  static constexpr int POS = 16 * PROW * 4;                   // the CTA's pos (+ bias) slice, fp32
   static constexpr int SMEM = NT * 32 * 8 + POS + WARPS * WBUF;
   static_assert((TROW % 128) == 64, "staged rows must alternate 64-byte bank halves");
 };
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
   constexpr int NT = PM::NT, TROW = PM::TROW;
   extern __shared__ __align__(128) uint8_t psm[];
   uint2* sB = reinterpret_cast<uint2*>(psm);  // [NT][32 lanes]
-  float* sPos = reinterpret_cast<float*>(psm + NT * 32 * 8);  // [16][HID]: bias + pos of this CTA's tokens
+  float* sPos = reinterpret_cast<float*>(psm + NT * 32 * 8);  // [16][PROW]: bias + pos of this CTA's tokens
   const uint32_t* pw32 = reinterpret_cast<const uint32_t*>(pw);  // [HID][8] bf16 pairs
   const int gw = HW / P, T = gw * gw, TG = T / 16;
   const int tg = blockIdx.x % TG, tau0 = tg * 16;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
     const int r = idx / (HID / 4), c4 = idx % (HID / 4);
     const float4 pv = __ldg(reinterpret_cast<const float4*>(pos + (int64_t)(tau0 + r) * HID) + c4);
     const float4 bv = __ldg(reinterpret_cast<const float4*>(pb) + c4);
-    reinterpret_cast<float4*>(sPos)[idx] = make_float4(bv.x + pv.x, bv.y + pv.y, bv.z + pv.z, bv.w + pv.w);
+    reinterpret_cast<float4*>(sPos + r * PM::PROW)[c4] = make_float4(bv.x + pv.x, bv.y + pv.y, bv.z + pv.z, bv.w + pv.w);
   }
   __syncthreads();
   // weights and the positional slice are no kernel's output: staged above under the previous
@@ -296,8 +298,8 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
   float* sStat = reinterpret_cast<float*>(sY + 16 * TROW);      // [16][rstd, -mean * rstd]
   const int64_t rows = total_tokens / T;
   const int64_t rstride = (int64_t)(gridDim.x / TG) * PM::WARPS;
-  const float* pos0 = sPos + g * HID + 8 * c;
-  const float* pos1 = pos0 + 8 * HID;
+  const float* pos0 = sPos + g * PM::PROW + 8 * c;
+  const float* pos1 = pos0 + 8 * PM::PROW;
   uint8_t* y0 = sY + g * TROW + 16 * c;
   uint8_t* y1 = y0 + 8 * TROW;
   // x of this lane for latent row ni: (row g, k 2c) (row g+8, k 2c) (row g, k 2c+8) (row g+8, k 2c+8)
