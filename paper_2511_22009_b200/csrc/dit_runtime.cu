@@ -241,9 +241,10 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 // (the long-scoreboard stall that bounded the previous version).  The next group's x is
 // prefetched into registers.  The 16 residual rows are staged in shared memory as NSEG = HID/192
 // segments of 208 elements (416 B: consecutive rows alternate 64-byte bank halves, conflict-
-// free 16-byte writes) and leave by one TMA store (the 16 zero-padding elements of a segment
-// are out of bounds of the [tokens * NSEG, 192] tensor map, so they are not written); LN +
-// modulate runs in a copy-out layout from the staged bf16 residual (coalesced 8-byte lanes).
+// free 16-byte writes); the copy-out loop reads them back in a row-contiguous layout (8 bytes
+// per lane) and writes both the residual and LN + modulate with coalesced stores.  (The residual
+// used to leave by a TMA store of the staged rows; waiting for that store to have read the
+// buffer before the next row cost 5%.)
 template <int HID>
 struct PatchMma {
   static constexpr int NT = HID / 8;
@@ -267,7 +268,7 @@ template <int HID>
 __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_kernel(
     const float* __restrict__ x, int64_t lat_rows, int HW, int P, int C, const __nv_bfloat16* __restrict__ pw,
     const float* __restrict__ pb, const float* __restrict__ pos, const float* __restrict__ mod, int64_t mod_stride,
-    float ln_eps, const __grid_constant__ CUtensorMap tmRes, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens,
+    float ln_eps, __nv_bfloat16* __restrict__ xres, __nv_bfloat16* __restrict__ xmod, int64_t total_tokens,
     int pdl) {
   using PM = PatchMma<HID>;
   constexpr int NT = PM::NT, TROW = PM::TROW;
@@ -320,7 +321,6 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
   for (; ni < rows; ni += rstride) {
     // (the bulk wait comes before the next row's x loads: it compiles to a scoreboard wait that
     // would otherwise also wait for those loads)
-    if (lane == 0) bulk_wait_read<0>();  // the previous row's residual store has left sY
     __syncwarp();
     uint32_t ahi[4], alo[4];
 #pragma unroll
@@ -400,13 +400,8 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
       sStat[2 * (g + 8)] = rs1;
       sStat[2 * (g + 8) + 1] = -mean1 * rs1;
     }
-    fence_proxy_async_smem();  // the staged residual is read by the TMA store (async proxy)
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(&tmRes, sY, 0, (int)(tok0 * PM::NSEG));
-      bulk_commit();
-    }
-    // copy-out of LN + modulate: 8 B (4 columns) per lane and row, each lane on fixed columns 4k
+    __syncwarp();  // staged rows and statistics visible to the whole warp
+    // copy-out of the residual and of LN + modulate: 8 B (4 columns) per lane and row, each lane on fixed columns 4k
 #pragma unroll 2
     for (int row = 0; row < 16; ++row) {
       const float2 r2 = make_float2(sStat[2 * row], sStat[2 * row]);
@@ -422,11 +417,11 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
                                      make_float2(sh[jj].z, sh[jj].w));
         *reinterpret_cast<uint2*>(xmod + (tok0 + row) * HID + 4 * k) =
             make_uint2(pack_bf16(ya.x, ya.y), pack_bf16(yb.x, yb.y));
+        *reinterpret_cast<uint2*>(xres + (tok0 + row) * HID + 4 * k) = v;  // the residual itself
       }
     }
     __syncwarp();  // staged rows / stats consumed before the next row overwrites them
   }
-  if (lane == 0) bulk_wait<0>();
 }
 
 // ============================================================ K4: LayerNorm + adaLN modulate (wide rows)
@@ -768,7 +763,6 @@ struct sf_dit {
   std::vector<GemmMaps> g_qkv, g_proj, g_fc1, g_fc2;  // [depth]
   AttnMaps attn_maps;
   CUtensorMap fin_x, fin_w;  // final layer: xmod / final weight rows as 208-wide segment boxes
-  CUtensorMap pe_res;        // patch embed: xres as 208-wide segment boxes (TMA store)
   // One instantiated graph per distinct argument set of sf_dit_stream_step: every pointer and
   // value the capture bakes into a launch is part of the key, so a replay is always the launch
   // sequence an eager call with the same arguments would enqueue.  Owners release their graphs
@@ -954,7 +948,7 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;
   if (launch_kernel(kern, dim3((unsigned)(TG * per)), dim3(32 * wpb), sm, st, x, lat_rows, c.latent_hw, c.patch, c.in_ch,
                     (const __nv_bfloat16*)h->w.patch_w, (const float*)h->w.patch_b, (const float*)h->w.pos_embed,
-                    (const float*)h->mod, h->mod_stride, c.ln_eps, h->pe_res, h->xmod, tokens, g_pdl ? 1 : 0) != cudaSuccess)
+                    (const float*)h->mod, h->mod_stride, c.ln_eps, h->xres, h->xmod, tokens, g_pdl ? 1 : 0) != cudaSuccess)
     return SF_ERR_CUDA;
   mark(h, P_PATCH, st);
   return cuda_status();
@@ -1043,9 +1037,6 @@ int sf_dit_create(const sf_dit_config* cfg, const sf_dit_weights* w, int64_t max
     }
   }
   rc |= make_attn_maps(&h->attn_maps, h->q, h->k, h->vt, max_rows, c.heads, h->tokens, c.hidden / c.heads);
-  // [rows, HID] -> [rows * HID/192, 192], 208-wide boxes of 16 rows' segments (same view as the final layer)
-  rc |= make_tmap_bf16_2d(&h->pe_res, h->xres, 192, (uint64_t)max_rows * h->tokens * (c.hidden / 192), 192, 208,
-                          16 * (c.hidden / 192), 0);
   if (c.hidden == 384) {
     rc |= make_final_map<384>(&h->fin_x, h->xmod, max_rows * h->tokens);
     rc |= make_final_map<384>(&h->fin_w, w->final_w, 16);
