@@ -250,7 +250,8 @@ struct PatchMma {
   static constexpr int NT = HID / 8;
   static constexpr int NSEG = HID / 192;
   static constexpr int TROW = NSEG * 416;                     // staged row (bytes)
-  static constexpr int WARPS = HID <= 384 ? 5 : 2;            // per CTA (2 CTAs per SM at hidden 384)
+  static constexpr int WARPS = HID <= 384 ? 5 : 2;            // per CTA
+  static constexpr int CPS = HID <= 384 ? 2 : 1;              // resident CTAs per SM (shared-memory bound)
   static constexpr int WBUF = 16 * TROW + 16 * 2 * 4;         // per warp: 16 rows + (mean, rstd) x 16
   static constexpr int PROW = HID + 4;                        // pos row (floats), padded: the LDS.128 of rows
                                                               // g and g+1 land on disjoint banks (was 2-way)
@@ -278,12 +279,17 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
   const uint32_t* pw32 = reinterpret_cast<const uint32_t*>(pw);  // [HID][8] bf16 pairs
   const int gw = HW / P, T = gw * gw, TG = T / 16;
   const int tg = blockIdx.x % TG, tau0 = tg * 16;
-  for (int idx = threadIdx.x; idx < NT * 32; idx += blockDim.x) {
+  // (compile-time trip counts, fully unrolled: every load of the prologue is in flight at once
+  // instead of ~10 dependent L2 round trips per thread)
+  constexpr int NTHR = 32 * PM::WARPS;
+#pragma unroll
+  for (int idx = threadIdx.x; idx < NT * 32; idx += NTHR) {
     const int tile = idx / 32, gg = (idx % 32) / 4, cc = idx % 4;
     const int n = 32 * (tile / 4) + 8 * (gg >> 1) + 2 * (tile % 4) + (gg & 1);  // permuted weight row
     sB[idx] = make_uint2(pw32[n * 8 + cc], pw32[n * 8 + 4 + cc]);
   }
-  for (int idx = threadIdx.x; idx < 16 * HID / 4; idx += blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < 16 * HID / 4; idx += NTHR) {
     const int r = idx / (HID / 4), c4 = idx % (HID / 4);
     const float4 pv = __ldg(reinterpret_cast<const float4*>(pos + (int64_t)(tau0 + r) * HID) + c4);
     const float4 bv = __ldg(reinterpret_cast<const float4*>(pb) + c4);
@@ -942,7 +948,7 @@ static int launch_patch(sf_dit* h, const float* x, int64_t lat_rows, int64_t row
   // CTA c: token group c % TG of latent rows c / TG + k * (CTAs / TG); as many row blocks per
   // group as fill the resident CTA slots (smem-limited: 2 per SM at hidden 384, 1 at 1152)
   const int TG = h->tokens / 16;
-  const int64_t slots = c.hidden == 384 ? 2 * 148 : 148;
+  const int64_t slots = c.hidden == 384 ? PatchMma<384>::CPS * 148 : 148;
   int64_t per = std::max<int64_t>(1, slots / TG);
   per = std::min<int64_t>(per, (rows + wpb - 1) / wpb);
   auto kern = c.hidden == 384 ? patch_embed_ln_mma_kernel<384> : patch_embed_ln_mma_kernel<1152>;

@@ -12,7 +12,7 @@ def t(fn, bytes_, name):
         fn()
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(f"{name:12s} {bytes_ / ms / 1e9:8.1f} GB/s ({ms*1e3:.1f} us for {bytes_/1e6:.0f} MB)")
+    print(f"{name:12s} {bytes_ / ms / 1e6:8.1f} GB/s ({ms*1e3:.1f} us for {bytes_/1e6:.0f} MB)")
 t(lambda: x.fill_(1.0), 2 * n, "write-only")
 t(lambda: y.sum(), 2 * n, "read-only")
 t(lambda: x.copy_(y), 4 * n, "copy r+w")
