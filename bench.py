@@ -63,6 +63,43 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+# The driver launches one rank per GPU over NCCL.  SF_BENCH_DIST_BACKEND=gloo (tests only) lets
+# several ranks share one GPU (NCCL refuses duplicate devices), so the N > 1 path -- barrier,
+# max-over-ranks timing, frame gather -- runs on a single-GPU box; small tensors for the
+# collectives then live on the host.
+DIST_BACKEND = os.environ.get("SF_BENCH_DIST_BACKEND", "nccl")
+
+
+def dist_setup(world: int, local: int) -> int:
+    """Bind this rank's GPU and join the process group; returns the CUDA device index."""
+    import torch
+    import torch.distributed as dist
+
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(DIST_BACKEND)
+    return dev
+
+
+def coll_device() -> str:
+    return "cuda" if DIST_BACKEND == "nccl" else "cpu"
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device=coll_device())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 MODELS = {
     "mock": ("SeededMockModel", "reference SeededMockModel (blake2b row key + splitmix64), D=16384, no network"),
     "s2": ("DiT-S/2", "DiT-S/2 (depth 12, hidden 384, 6 heads, patch 2, 1024 tokens)"),
@@ -120,9 +157,7 @@ def run_mock(args):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = dist_setup(world, local)
     from paper_2511_22009_b200.build import build
 
     build()
@@ -156,13 +191,10 @@ def run_mock(args):
         if world > 1:
             dist.barrier()
         total = ev[0].elapsed_time(ev[K])
-        if world > 1:
-            t = torch.tensor([total], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
+        total = max_over_ranks(total, world)
         return total, [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
 
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     clocks.start()
     total_ms, step_ms = timed(sb.launch, args.steps)
     clk = clocks.stop()
@@ -411,9 +443,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = dist_setup(world, local)
     from paper_2511_22009_b200.build import build
 
     build()
@@ -449,13 +479,10 @@ def main():
             dist.barrier()
         steps = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
         total = ev[0].elapsed_time(ev[K])
-        if world > 1:
-            t = torch.tensor([total], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total = float(t.item())
+        total = max_over_ranks(total, world)
         return total, steps
 
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     j0 = sb.j
     clocks.start()
     total_ms, step_ms = timed(sb.launch, args.steps)
@@ -557,7 +584,7 @@ def main():
             sb.launch()
             fw.record()
         allf, ids = fw.gather()
-        cnt = reduce_counts([S * args.steps, sb.stats[0].model_calls], "cuda")
+        cnt = reduce_counts([S * args.steps, sb.stats[0].model_calls], coll_device())
         gathered = {"window_steps": n, "frames_gathered": int(allf.shape[0] * allf.shape[1]),
                     "frame_ids_valid": int((ids >= 0).sum().item()), "frames_emitted_timed_total": cnt[0]}
 
