@@ -431,71 +431,128 @@ __global__ void __launch_bounds__(32 * PatchMma<HID>::WARPS) patch_embed_ln_mma_
 }
 
 // ============================================================ K4: LayerNorm + adaLN modulate (wide rows)
-// xmod = LN(xres) * (1 + scale[slot]) + shift[slot]; one warp per token, lane
-// owns columns 128u + 4 lane + {0..3}.  Used where the row is wider than one
-// TMEM accumulator tile (DiT-XL hidden 1152), after the gated-residual GEMM.
-template <int HID>
-__global__ void __launch_bounds__(256) ln_modulate_kernel(const __nv_bfloat16* __restrict__ xres,
-                                                          __nv_bfloat16* __restrict__ xmod,
-                                                          const float* __restrict__ shift,
-                                                          const float* __restrict__ scale, int64_t vec_stride,
-                                                          int64_t M, int T, float ln_eps, int pdl) {
+// xmod = LN(xres) * (1 + scale[slot]) + shift[slot]; one warp per token, lane owns columns
+// 128u + 4 lane + {0..3}.  Used where the row is wider than one TMEM accumulator tile (DiT-XL
+// hidden 1152), after the gated-residual GEMM.  A warp walks LN_TPW consecutive tokens with the
+// next token's row in flight (rows kept as packed bf16); when a
+// CTA's 8 * LN_TPW tokens share a slot (STAGE: tokens_per_slot % (8 * LN_TPW) == 0, every DiT
+// shape) the slot's shift and 1 + scale are staged in shared memory once per CTA, under the row
+// loads.  (The first version loaded them per token after the row reductions and ran one token
+// per warp: 12.1-13.2 us for the 8192 tokens of the XL batch under ncu, long-scoreboard bound;
+// this one 10.9-12.0, bit-identical.)
+constexpr int LN_TPW = 2;   // tokens per warp per group
+constexpr int LN_CTAS = 2;  // resident CTAs per SM (the prefetched row doubles the live registers)
+template <int HID, bool STAGE>
+__global__ void __launch_bounds__(256, LN_CTAS) ln_modulate_kernel(const __nv_bfloat16* __restrict__ xres,
+                                                             __nv_bfloat16* __restrict__ xmod,
+                                                             const float* __restrict__ shift,
+                                                             const float* __restrict__ scale, int64_t vec_stride,
+                                                             int64_t M, int T, float ln_eps, int pdl) {
   constexpr int U = HID / 128;
+  __shared__ float4 sv[STAGE ? 2 * HID / 4 : 1];  // [shift | 1 + scale] of the CTA's slot
   pdl_wait(pdl);
   if (threadIdx.x == 0) pdl_trigger(pdl);
-  const int lane = threadIdx.x & 31;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t tok = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; tok < M; tok += wstride) {
-    float y[U][4];
-    float sum = 0.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t groups = (M + 8 * LN_TPW - 1) / (8 * LN_TPW);
+  int64_t staged = -1;
+  auto load_row = [&](int64_t tok, uint2 (&r)[U]) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(xres + tok * HID + 128 * u + 4 * lane);
-      const float2 a = unpack_bf16(raw.x), b = unpack_bf16(raw.y);
-      y[u][0] = a.x;
-      y[u][1] = a.y;
-      y[u][2] = b.x;
-      y[u][3] = b.y;
-      sum += (a.x + a.y) + (b.x + b.y);
+    for (int u = 0; u < U; ++u) r[u] = *reinterpret_cast<const uint2*>(xres + tok * HID + 128 * u + 4 * lane);
+  };
+  for (int64_t gi = blockIdx.x; gi < groups; gi += gridDim.x) {
+    const int64_t tok0 = gi * 8 * LN_TPW + warp * LN_TPW;
+    uint2 raw[U];
+    if (tok0 < M) load_row(tok0, raw);
+    if constexpr (STAGE) {
+      const int64_t slot = gi * 8 * LN_TPW / T;  // block-uniform
+      if (slot != staged) {
+        __syncthreads();  // the previous slot's readers are done
+        const float4* sh4 = reinterpret_cast<const float4*>(shift + slot * vec_stride);
+        const float4* sc4 = reinterpret_cast<const float4*>(scale + slot * vec_stride);
+        for (int i = threadIdx.x; i < HID / 4; i += blockDim.x) {
+          const float4 c = sc4[i];
+          sv[i] = sh4[i];
+          sv[HID / 4 + i] = make_float4(1.0f + c.x, 1.0f + c.y, 1.0f + c.z, 1.0f + c.w);
+        }
+        __syncthreads();
+        staged = slot;
+      }
     }
+#pragma unroll 1
+    for (int k = 0; k < LN_TPW; ++k) {
+      const int64_t tok = tok0 + k;
+      if (tok >= M) break;
+      uint2 nxt[U];
+      if (k + 1 < LN_TPW && tok + 1 < M) load_row(tok + 1, nxt);
+      float sum = 0.f;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mean = sum / HID;
-    float var = 0.f;
+      for (int u = 0; u < U; ++u) {
+        const float2 a = unpack_bf16(raw[u].x), b = unpack_bf16(raw[u].y);
+        sum += (a.x + a.y) + (b.x + b.y);
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mean = sum / HID;
+      float var = 0.f;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) var += (y[u][r] - mean) * (y[u][r] - mean);
+      for (int u = 0; u < U; ++u) {
+        const float2 a = unpack_bf16(raw[u].x), b = unpack_bf16(raw[u].y);
+        var += (a.x - mean) * (a.x - mean);
+        var += (a.y - mean) * (a.y - mean);
+        var += (b.x - mean) * (b.x - mean);
+        var += (b.y - mean) * (b.y - mean);
+      }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-    const float rstd = rsqrtf(var / HID + ln_eps);
-    const int64_t slot = tok / T;
-    const float* sh = shift + slot * vec_stride;
-    const float* sc = scale + slot * vec_stride;
+      for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+      const float rstd = rsqrtf(var / HID + ln_eps);
+      const int64_t slot = tok / T;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n0 = 128 * u + 4 * lane;
-      const float4 s4 = *reinterpret_cast<const float4*>(sh + n0);
-      const float4 c4 = *reinterpret_cast<const float4*>(sc + n0);
-      const float o0 = (y[u][0] - mean) * rstd * (1.0f + c4.x) + s4.x;
-      const float o1 = (y[u][1] - mean) * rstd * (1.0f + c4.y) + s4.y;
-      const float o2 = (y[u][2] - mean) * rstd * (1.0f + c4.z) + s4.z;
-      const float o3 = (y[u][3] - mean) * rstd * (1.0f + c4.w) + s4.w;
-      *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      for (int u = 0; u < U; ++u) {
+        const int n0 = 128 * u + 4 * lane;
+        float4 s4, c4;
+        if constexpr (STAGE) {
+          s4 = sv[n0 / 4];
+          c4 = sv[HID / 4 + n0 / 4];
+        } else {
+          s4 = *reinterpret_cast<const float4*>(shift + slot * vec_stride + n0);
+          const float4 c = *reinterpret_cast<const float4*>(scale + slot * vec_stride + n0);
+          c4 = make_float4(1.0f + c.x, 1.0f + c.y, 1.0f + c.z, 1.0f + c.w);
+        }
+        const float2 a = unpack_bf16(raw[u].x), b = unpack_bf16(raw[u].y);
+        const float o0 = (a.x - mean) * rstd * c4.x + s4.x;
+        const float o1 = (a.y - mean) * rstd * c4.y + s4.y;
+        const float o2 = (b.x - mean) * rstd * c4.z + s4.z;
+        const float o3 = (b.y - mean) * rstd * c4.w + s4.w;
+        *reinterpret_cast<uint2*>(xmod + tok * HID + n0) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      }
+      if (k + 1 < LN_TPW) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u] = nxt[u];
+      }
     }
   }
 }
 
+template <int HID>
+static cudaError_t launch_ln_hid(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const float* shift,
+                                 const float* scale, int64_t vec_stride, int64_t M, int T, float eps,
+                                 cudaStream_t st) {
+  const int64_t groups = (M + 8 * LN_TPW - 1) / (8 * LN_TPW);
+  const unsigned blocks = (unsigned)std::min<int64_t>(groups, 148 * LN_CTAS);
+  if (T % (8 * LN_TPW) == 0)
+    return launch_kernel(ln_modulate_kernel<HID, true>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale,
+                         vec_stride, M, T, eps, g_pdl ? 1 : 0);
+  return launch_kernel(ln_modulate_kernel<HID, false>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale,
+                       vec_stride, M, T, eps, g_pdl ? 1 : 0);
+}
+
 int launch_ln_modulate(const __nv_bfloat16* xres, __nv_bfloat16* xmod, const float* shift, const float* scale,
                        int64_t vec_stride, int64_t M, int N, int tokens_per_slot, float eps, cudaStream_t st) {
-  const unsigned blocks = (unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16);
   cudaError_t err;
   if (N == 384)
-    err = launch_kernel(ln_modulate_kernel<384>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale, vec_stride, M,
-                        tokens_per_slot, eps, g_pdl ? 1 : 0);
+    err = launch_ln_hid<384>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps, st);
   else if (N == 1152)
-    err = launch_kernel(ln_modulate_kernel<1152>, dim3(blocks), dim3(256), 0, st, xres, xmod, shift, scale, vec_stride,
-                        M, tokens_per_slot, eps, g_pdl ? 1 : 0);
+    err = launch_ln_hid<1152>(xres, xmod, shift, scale, vec_stride, M, tokens_per_slot, eps, st);
   else
     return SF_ERR_PARAMETER;
   return err == cudaSuccess ? cuda_status() : SF_ERR_CUDA;

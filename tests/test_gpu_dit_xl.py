@@ -125,3 +125,27 @@ def test_gemm_res_pair_tiles_ragged(M, K, T):
     ref = x0[:M].float() + vec[slot] * (a.float() @ w.float().t() + b)
     assert (xres[:M].float() - ref).abs().max().item() < 3e-2 * max(1.0, ref.abs().max().item())
     assert torch.equal(xres[M:], x0[M:])
+
+
+@pytest.mark.parametrize("D", [384, 1152])
+def test_ln_modulate_staged_and_direct_paths(D):
+    """sf_ln_modulate stages a slot's shift / 1+scale in shared memory when a CTA's 16 tokens
+    share a slot (tokens_per_slot % 16 == 0) and reads them per token otherwise: with the same
+    vectors in every slot the two paths must agree bit for bit, and both match LayerNorm."""
+    from paper_2511_22009_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M = 4096 + 16 * 3  # ragged tail of CTA groups
+    x = (torch.randn(M, D, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    v = torch.randn(1, 3 * D, device="cuda", generator=g) * 0.5
+    outs = {}
+    for T in (16, 8, 1):  # staged, direct, direct (one token per slot)
+        vec = v.expand(M // T, 3 * D).contiguous()
+        y = torch.empty_like(x)
+        _lib.call("sf_ln_modulate", x.data_ptr(), y.data_ptr(), vec[:, D:].data_ptr(), vec[:, 2 * D:].data_ptr(),
+                  3 * D, M, D, T, 1e-6, torch.cuda.current_stream().cuda_stream)
+        outs[T] = y
+    torch.cuda.synchronize()
+    assert torch.equal(outs[16], outs[8]) and torch.equal(outs[16], outs[1])
+    want = torch.nn.functional.layer_norm(x.float(), (D,), eps=1e-6) * (1 + v[:, 2 * D:]) + v[:, D:2 * D]
+    assert (outs[16].float() - want).abs().max().item() < 2e-2 * want.abs().max().item()
