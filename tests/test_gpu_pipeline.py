@@ -166,3 +166,48 @@ def test_mixed_guidance_scales_match_independent_runs(sf, dtype):
         run = O.run_stream(m, n, fn, 300 + s, osch, D, dtype=dtype)
         for r in out[s]:
             assert np.array_equal(r.latent, run.latents[r.id]), (s, r.id)
+
+
+def _random_cases(count=40, seed=2026):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(count):
+        S = int(rng.integers(1, 8))
+        n = int(rng.integers(1, 6))
+        k = int(rng.integers(1, 6))
+        m = int(rng.integers(1, 10))
+        D = int(rng.choice([8, 100, 256, 1000, 4096]))
+        dtype = np.float64 if rng.random() < 0.5 else np.float32
+        ws = [1.0 if rng.random() < 0.4 else float(np.round(rng.uniform(0.0, 9.0), 3)) for _ in range(S)]
+        has_neg = [bool(rng.random() < 0.5) for _ in range(S)]
+        seeds = [int(v) for v in rng.integers(0, 2**31, size=S)]  # arbitrary, non-consecutive
+        cases.append((i, S, n, k, m, D, dtype, ws, has_neg, seeds))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_cases(), ids=lambda c: f"case{c[0]}")
+def test_random_stream_batches_match_oracle(sf, case):
+    """Seeded random configurations (streams, steps per generation, windows, generations, latent
+    size, dtype, per-stream guidance with and without negative embeddings, arbitrary per-stream
+    seeds): one device batch == independent oracle runs, bit for bit, with the reference's
+    call counts."""
+    _, S, n, k, m, D, dtype, ws, has_neg, seeds = case
+    sched = sf.build_time_window_schedule(num_windows=k, inference_steps=n)
+    model = sf.SeededMockModel(dim=D, seed=17)
+    rng = np.random.default_rng(seeds[0] % 1000)
+    embs = [rng.standard_normal(8) for _ in range(S)]
+    negs = [rng.standard_normal(8) if has_neg[s] else None for s in range(S)]
+    conds = [sf.make_conditioning(embs[s], guidance_scale=ws[s], negative_embedding=negs[s]) for s in range(S)]
+    sb = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, m=m, dtype=dtype)
+    out = sb()
+    osch = O.make_schedule(num_windows=k, steps=n)
+    for s in range(S):
+        fn = lambda ids, ts, x, s=s: O.guided_mock_eps(17, ids, ts, embs[s], negs[s], ws[s], D)  # noqa: E731
+        run = O.run_stream(m, n, fn, seeds[s], osch, D, dtype=dtype)
+        assert [r.id for r in out[s]] == run.order, s
+        for r in out[s]:
+            assert r.latent.dtype == dtype
+            assert np.array_equal(r.latent, run.latents[r.id]), (s, r.id)
+        st = sb.stats[s]
+        assert st.step_stats.param_evals == m * n
+        assert st.model_calls == m + n - 1 and st.decodes == m
