@@ -248,3 +248,27 @@ def test_batch_of_streams_equals_single_stream_batches():
         assert [r.id for r in one] == [r.id for r in big[s]]
         for a, b in zip(one, big[s]):
             assert np.array_equal(a.latent, b.latent), (s, a.id)
+
+
+@pytest.mark.parametrize("S,n,m", [(3, 2, 4), (6, 4, 5)])
+def test_batch_of_guided_streams_equals_single_stream_batches(S, n, m):
+    """Per-stream guidance scales (1.0 included) with and without negative embeddings: one guided
+    DiT batch (2 S n network rows: 12 rows = the small-batch PDL path, 48 rows = plain launches)
+    gives each stream the frames of its own single-stream batch, bit for bit."""
+    import paper_2511_22009_b200 as sf
+    from paper_2511_22009_b200.dit import DIT_S2
+
+    model = sf.DiTVelocityModel(DIT_S2, seed=5, max_rows=2 * S * n, bias_std=0.02)
+    sched = sf.build_time_window_schedule(num_windows=3, inference_steps=n)
+    rng = np.random.default_rng(S * 10 + n)
+    ws = [1.0, 4.0, 7.5, 2.5, 1.0, 6.0][:S]
+    conds = [sf.make_conditioning(rng.standard_normal(8), guidance_scale=ws[s],
+                                  negative_embedding=rng.standard_normal(8) if s % 2 else None) for s in range(S)]
+    seeds = [int(v) for v in rng.integers(0, 2**31, size=S)]
+    big = sf.StreamBatch(model, sched, n, num_streams=S, cond=conds, seed=seeds, m=m, dtype=np.float32)()
+    for s in range(S):
+        one = sf.StreamBatch(model, sched, n, num_streams=1, cond=[conds[s]], seed=[seeds[s]], m=m,
+                             dtype=np.float32)()[0]
+        assert [r.id for r in one] == [r.id for r in big[s]]
+        for a, b in zip(one, big[s]):
+            assert np.array_equal(a.latent, b.latent), (s, a.id)
