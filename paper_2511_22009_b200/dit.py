@@ -219,6 +219,9 @@ class DeviceDiT:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
+            # null the handle first: objects that still reference this model (a StreamBatch in the
+            # same garbage cycle, finalized after it) then see a NULL handle, never a freed one
+            self._h = C.c_void_p()
             try:
                 _lib.fn("sf_dit_destroy")(h)
             except Exception:

@@ -246,7 +246,9 @@ class StreamBatch:
         # drop the CUDA graphs captured over this batch's buffers before they are freed
         if getattr(self, "kind", None) == "dit" and getattr(self, "use_graph", False):
             try:
-                _lib.fn("sf_dit_graph_release")(self.model.device_model.handle, self.ctl.data_ptr())
+                h = self.model.device_model.handle
+                if h.value:  # NULL once the model's runtime handle is destroyed (graphs went with it)
+                    _lib.fn("sf_dit_graph_release")(h, self.ctl.data_ptr())
             except Exception:
                 pass
 

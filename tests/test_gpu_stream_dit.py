@@ -272,3 +272,37 @@ def test_batch_of_guided_streams_equals_single_stream_batches(S, n, m):
         assert [r.id for r in one] == [r.id for r in big[s]]
         for a, b in zip(one, big[s]):
             assert np.array_equal(a.latent, b.latent), (s, a.id)
+
+
+def test_finalizer_order_model_before_batch():
+    """A DiT StreamBatch and its model collected in either order (as a garbage cycle at interpreter
+    shutdown may do): the model's finalizer destroys the runtime handle and nulls it, so the
+    batch's finalizer, run afterwards, sees NULL instead of a freed handle, and the model's own
+    finalizer running again is a no-op (subprocess: a use-after-free would kill the interpreter)."""
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np, torch
+import paper_2511_22009_b200 as sf
+from paper_2511_22009_b200.dit import DIT_S2
+model = sf.DiTVelocityModel(DIT_S2, seed=1, max_rows=8)
+sched = sf.build_time_window_schedule(inference_steps=4)
+sb = sf.StreamBatch(model, sched, 4, num_streams=2, cond=sf.make_conditioning(np.ones(8)), seed=0,
+                    dtype=np.float32, noise="device", use_graph=True)
+for _ in range(3):
+    sb.launch()
+torch.cuda.synchronize()
+dm = model.device_model
+dm.__del__()      # the model first ...
+sb.__del__()      # ... then the batch's graph release: must see a NULL handle
+dm.__del__()      # and a second finalizer call must not destroy again
+del sb, model, dm
+import gc; gc.collect()
+print("finalizers ok")
+'''
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "finalizers ok" in r.stdout, (r.returncode, r.stdout[-500:], r.stderr[-2000:])
