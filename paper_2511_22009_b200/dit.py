@@ -218,11 +218,12 @@ class DeviceDiT:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            # null the handle first: objects that still reference this model (a StreamBatch in the
-            # same garbage cycle, finalized after it) then see a NULL handle, never a freed one
-            self._h = C.c_void_p()
+        hv = getattr(h, "value", None)
+        if hv:
+            # null the handle object in place first: holders of it (a StreamBatch in the same
+            # garbage cycle, finalized after this model) then see NULL, never a freed handle
+            h.value = None
             try:
-                _lib.fn("sf_dit_destroy")(h)
+                _lib.fn("sf_dit_destroy")(hv)
             except Exception:
                 pass
