@@ -119,7 +119,8 @@ struct GemmCfg {
   // RES: one 64-column residual chunk per buffer, as many buffers as the warp has chunks (a
   // second buffer for one-chunk warps would only cost operand-ring stages: 4 -> 6 at BN = 192);
   // GELU at BN = 256: one buffer per warp (its two 32-column chunks take turns), 4 -> 5 stages
-  static constexpr int OUT_NBUF = LN_RING                                          ? BN / (EPI_WARPS / 4) / 32
+  static constexpr int OUT_NBUF = KIND == EPI_F32                                  ? 0  // writes fp32 directly
+                                  : LN_RING                                        ? BN / (EPI_WARPS / 4) / 32
                                   : KIND == EPI_RES                                ? BN / (EPI_WARPS / 4) / 64
                                   : (KIND == EPI_QKV && BN == 192 && TILE_GROUPS == 1) ? 3
                                   : (KIND == EPI_GELU && BN == 256)                 ? 1  // 5 stages, not 4
