@@ -10,7 +10,7 @@ import ctypes as C
 import os
 import re
 
-from .errors import InvariantError, ParameterError, StateError, TimeDomainError
+from .errors import STATUS_ERRORS
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SF_LIB_PATH") or os.path.join(_HERE, "libstreamflow.so")  # override: diagnostics
@@ -101,12 +101,8 @@ def fn(name: str):
     return f
 
 
-_ERRS = {
-    SF_ERR_PARAMETER: ParameterError,
-    SF_ERR_TIME_DOMAIN: TimeDomainError,
-    SF_ERR_INVARIANT: InvariantError,
-    SF_ERR_STATE: StateError,
-}
+_ERRS = STATUS_ERRORS
+assert set(_ERRS) == {SF_ERR_PARAMETER, SF_ERR_TIME_DOMAIN, SF_ERR_INVARIANT, SF_ERR_STATE}
 
 
 def check(code: int, what: str) -> None:
