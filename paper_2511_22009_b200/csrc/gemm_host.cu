@@ -240,4 +240,7 @@ int launch_gemm(int kind, int bn, const GemmMaps& maps, int M, int N, int K, con
 extern "C" int sf_gemm_trace_read(long long* dst) {
   return cudaMemcpyFromSymbol(dst, sf::g_gemm_trace, sizeof(long long) * 8 * 64) == cudaSuccess ? 0 : -1;
 }
+extern "C" int sf_gemm_cta_end_read(unsigned long long* dst) {
+  return cudaMemcpyFromSymbol(dst, sf::g_gemm_cta_end, sizeof(unsigned long long) * 1024) == cudaSuccess ? 0 : -1;
+}
 #endif

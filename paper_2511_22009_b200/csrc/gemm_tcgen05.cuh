@@ -25,6 +25,7 @@ namespace sf {
 #endif
 #if SF_GEMM_TRACE
 __device__ long long g_gemm_trace[8 * 64];
+__device__ unsigned long long g_gemm_cta_end[1024];  // %globaltimer at each CTA's end (ns, GPU-wide clock)
 #define GTR(role, idx)                                                               \
   do {                                                                               \
     if (blockIdx.x == 0 && (idx) < 64) g_gemm_trace[(role) * 64 + (idx)] = clock64(); \
@@ -835,6 +836,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI_WARPS, KIND, CTAS>::THREADS, 1
 
   tc_fence_before();
   __syncthreads();
+#if SF_GEMM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_cta_end[blockIdx.x] = t;
+  }
+#endif
   if constexpr (TWO_SM) cluster_sync_all();  // the pair's MMAs / barrier traffic are over
   if (warp == 1) {
     if constexpr (TWO_SM)
